@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — B200 GLM / TPA-SCD hot path on the BASELINE.json workload.
+
+Workload (configs[1], "C2"): L2-regularised logistic regression on a synthetic
+sparse matrix of 1,000,000 examples x 100,000 features with 40 nnz per
+example, trained by SCD in the dual (the reference kind `dual_l2_logistic`:
+columns are label-folded examples, d = 100k). The primal
+form named in BASELINE.json is a restated kind the reference lacks; the dual
+is the path the reference implements and pins.
+
+A "step" = one outer round = one full SCD epoch over every example
+(async TPA-SCD kernel) + the Delta v allreduce across ranks (NCCL, N > 1).
+value = epochs/s of the whole job (strong scaling: the same 1M-example dataset
+is column-partitioned over N ranks). Inputs are resident in HBM; the matrix
+(480 MB) exceeds the 126 MB L2, so no flush is needed between steps.
+
+e2e = the same metric through the reference-facing plugin C-ABI
+(glm_device_solve, host buffers: H2D of lin+base, D2H of delta_alpha+delta_v
+each step; + the host Delta v allreduce for N > 1).
+
+--impl reference times the CPU oracle port of the reference algorithm
+(oracle/, C + numpy) with all host threads (CoCoA over nproc workers, the
+reference's multi-process mode) on the same data.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SCD epochs/s + time to 1e-3 suboptimality, sparse LogReg, 1/2/4/8 B200"
+N_EX, D_FEAT, NNZ, BLOCK = 1_000_000, 100_000, 40, 125_000
+LAM = 1.0
+
+
+# ------------------------------------------------------------------ data
+def planted_w():
+    return np.random.default_rng(0xC2).standard_normal(D_FEAT)
+
+
+def gen_block(b, w):
+    """Block b of BLOCK examples: 40 distinct sorted features each, N(0,1)
+    values normalised per example, labels = sign(x.w + 0.3 noise), columns
+    folded by the label (cli.py:173-181 layout)."""
+    rng = np.random.default_rng([0xC2, b])
+    rows = np.sort(rng.integers(0, D_FEAT - NNZ + 1, size=(BLOCK, NNZ), dtype=np.int32),
+                   axis=1) + np.arange(NNZ, dtype=np.int32)
+    vals = rng.standard_normal((BLOCK, NNZ))
+    vals /= np.linalg.norm(vals, axis=1, keepdims=True)
+    score = np.einsum("ij,ij->i", vals, w[rows]) + 0.3 * rng.standard_normal(BLOCK)
+    y = np.where(score >= 0, 1.0, -1.0)
+    vals *= y[:, None]
+    return rows.reshape(-1), vals.reshape(-1), y
+
+
+def gen_columns(lo_block, hi_block):
+    w = planted_w()
+    parts = [gen_block(b, w) for b in range(lo_block, hi_block)]
+    rows = np.concatenate([p[0] for p in parts])
+    vals = np.concatenate([p[1] for p in parts])
+    y = np.concatenate([p[2] for p in parts])
+    n = len(y)
+    indptr = np.arange(0, n * NNZ + 1, NNZ, dtype=np.int64)
+    return indptr, rows, vals, y
+
+
+# ------------------------------------------------------------- utilities
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_scd_async_c2.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ CPU arm
+def cpu_arm(args, n_blocks=None, budget_s=15.0):
+    """The oracle port (reference algorithm: CoCoA over nproc host workers,
+    each a sequential damped_solve in C) on the same C2 data."""
+    import oracle
+    cores = os.cpu_count() or 1
+    nb = n_blocks or (N_EX // BLOCK)
+    indptr, rows, vals, _ = gen_columns(0, nb)
+    m = oracle.OMatrix(D_FEAT, indptr, rows, vals)
+    # one warm round then as many timed rounds as fit the budget
+    t0 = time.perf_counter()
+    oracle.train(m, 0, LAM, nodes=cores, epochs=1, seed=0, rounds=1, parallel=True,
+                 record_obj=False)
+    t_round = time.perf_counter() - t0
+    rounds = max(1, min(int(budget_s / max(t_round, 1e-3)), 50))
+    res = oracle.train(m, 0, LAM, nodes=cores, epochs=1, seed=0, rounds=rounds,
+                       parallel=True, record_obj=False)
+    per = float(np.mean(res["round_s"]))
+    frac = nb * BLOCK / N_EX
+    return {"value": frac / per, "unit": "epochs/s", "cores": cores, "kind": "port",
+            "sample": f"{rounds} CoCoA rounds (1 epoch each, K={cores} host workers, "
+                      f"C sequential SCD per worker) over {nb * BLOCK} of {N_EX} examples; "
+                      f"epochs/s scaled to the full dataset"}
+
+
+def reference_main(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    res = cpu_arm(args, budget_s=max(5.0, 2.0 * args.steps))
+    line = {"metric": METRIC, "value": res["value"], "unit": "epochs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / res["value"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": config_block(world),
+            "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": "epochs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(world):
+    return {"workload": "C2: L2 logistic regression (dual SCD, kind dual_l2_logistic), "
+                        "synthetic sparse 1M examples x 100k features, 40 nnz/example, "
+                        "lambda=1",
+            "n_examples": N_EX, "n_features": D_FEAT, "nnz_per_example": NNZ,
+            "nnz": N_EX * NNZ, "lambda": LAM, "epochs_per_round": 1,
+            "parallelism": f"CoCoA K={world} (one rank per GPU, NCCL Delta-v allreduce)",
+            "solver": "async TPA-SCD (group-per-coordinate, red.global.add.f64)",
+            "l2_flush": "inputs (480 MB matrix) larger than the 126 MB L2"}
+
+
+# ------------------------------------------------------------ GPU arm
+def ours_main(args):
+    import torch
+    world, rank, local = dist_setup()
+    import paper_1803_06333_b200 as g
+    from paper_1803_06333_b200 import _lib
+    from paper_1803_06333_b200.comm import NcclReducer
+    from paper_1803_06333_b200.data import DeviceMatrix
+    from paper_1803_06333_b200.solver import device_solve_host
+
+    n_blocks = N_EX // BLOCK
+    if n_blocks % world:
+        raise SystemExit(f"--gpus must divide {n_blocks}")
+    per = n_blocks // world
+    lo_b, hi_b = rank * per, (rank + 1) * per
+    indptr, rows, vals, y = gen_columns(lo_b, hi_b)
+    m_loc = len(y)
+    nnz_loc = int(indptr[-1])
+    dm = DeviceMatrix.from_csc(D_FEAT, indptr, rows, vals)
+    spec = g.ObjectiveSpec("dual_l2_logistic", LAM, N_EX, D_FEAT)
+    reducer = NcclReducer() if world > 1 else None
+    cfg = g.HierarchyConfig(nodes=world, devices=1, t1=10 ** 6, seed=0, epochs=1)
+
+    def make_engine():
+        return g.Engine(dm, spec, cfg, reducer=reducer, node_index=rank if world > 1 else None,
+                        mode="async", sync_solves=False, retry_budget=0,
+                        n_total=N_EX if world > 1 else None)
+
+    eng = make_engine()
+    wk = next(iter(eng.workers.values()))
+    lib = _lib.lib()
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        eng.outer_round()
+    torch.cuda.synchronize()
+    eng.check_solves()
+    if world > 1:
+        torch.distributed.barrier()
+    wk.solver.timing(True)
+    launches0 = lib.glm_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            eng.outer_round()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.glm_launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    ms_total = max_over_ranks(ms_total, world)
+    kern_ms, attempts = wk.solver.timing_read()
+    wk.solver.timing(False)
+    eng.check_solves()
+    res_state, _ = wk.solver.result()
+    ms_step = ms_total / args.steps
+    value = 1000.0 / ms_step
+
+    # roofline of the dominant kernel (scd_async): algorithmic bytes per launch
+    epoch_ms = kern_ms[1] / max(attempts, 1)
+    alg_bytes = 12 * nnz_loc + 36 * m_loc
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / (epoch_ms * 1e-3) / 1e9
+    ncu = load_ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu.get("traffic_bytes") if ncu else None,
+                "kernel": "scd_async (epoch kernel, incl. the d-sized view snapshot)",
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_model": "12*nnz + 36*n (SURVEY 8(d))", "kernel_ms": epoch_ms,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "step_breakdown_ms": {"permutation": kern_ms[0] / max(attempts, 1),
+                                      "epoch": epoch_ms,
+                                      "value_damping": kern_ms[2] / max(attempts, 1),
+                                      "step": ms_step}}
+
+    # -------- e2e through the reference-facing C-ABI with host buffers
+    e2e = e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world)
+
+    # -------- time to 1e-3 suboptimality (certified by the duality gap)
+    ttt = None
+    if not args.no_ttt:
+        eng2 = make_engine()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        obj0, gap0 = eng2.objective_and_gap()
+        rounds = 0
+        gap = gap0
+        obj = obj0
+        while gap > 1e-3 * abs(obj) and rounds < 200:
+            eng2.outer_round()
+            rounds += 1
+            obj, gap = eng2.objective_and_gap()
+        torch.cuda.synchronize()
+        ttt = {"seconds": time.perf_counter() - t0, "epochs": rounds,
+               "target": "duality gap <= 1e-3 * |F| (certifies relative suboptimality)",
+               "final_gap": gap, "final_objective": obj, "includes_gap_checks": True}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_arm(args, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {"metric": METRIC, "value": value, "unit": "epochs/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": config_block(world),
+                "coord_updates_per_s": value * N_EX,
+                "time_to_target": ttt, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+                "solver_state": {"retries_last_round": int(res_state.retries),
+                                 "epochs_run_last_round": int(res_state.epochs_run),
+                                 "damping": float(res_state.damping)}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world):
+    """Reference-facing plugin path: glm_device_solve with pinned host buffers
+    (the drop-in for Engine(chunk_runner=...), engine.py:228-229)."""
+    import ctypes
+
+    import torch
+    from paper_1803_06333_b200 import _lib
+    m = len(indptr) - 1
+    d = D_FEAT
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().glm_ctx_create(
+        torch.cuda.current_device(), _lib.CSC, d, m, indptr.ctypes.data_as(ctypes.c_void_p),
+        rows.ctypes.data_as(ctypes.c_void_p), vals.ctypes.data_as(ctypes.c_void_p),
+        ctypes.byref(h)), "glm_ctx_create")
+
+    def pinned(n):
+        return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+
+    lin, base, dl, dvb = pinned(d), pinned(m), pinned(m), pinned(d)
+    base[:] = 0.5
+    v0 = np.zeros(d)
+    lin[:] = v0 / LAM
+    sub = g.LocalSubproblem(spec=spec, lin=lin, quad=world / LAM, const=0.0, base=base,
+                            data=None, col_ids=np.arange(m))
+    gen_state = g.derive_seed(0, 0)
+    damping = 1.0
+    steps = max(3, args.steps // 2)
+    for _ in range(2):
+        out = device_solve_host(h, sub, gen_state, damping, 1, 1, out=(dl, dvb))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = device_solve_host(h, sub, gen_state, damping, 1, 1, out=(dl, dvb))
+        _lib.check(int(out[7]), "glm_device_solve")
+        if reducer is not None:
+            reducer.allreduce_sum(dvb)
+    el = time.perf_counter() - t0
+    el = max_over_ranks(el, world)
+    _lib.lib().glm_ctx_destroy(h)
+    return {"value": steps / el, "unit": "epochs/s",
+            "h2d_bytes_per_step": 8 * (d + m + 1), "d2h_bytes_per_step": 8 * (m + d),
+            "path": "glm_device_solve (host buffers, pinned) per rank"
+                    + (" + host Delta-v allreduce" if reducer is not None else ""),
+            "timer": "host wall clock around the plugin call (includes copies)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_main(args)
+    return ours_main(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

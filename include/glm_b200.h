@@ -1,0 +1,245 @@
+/*
+ * glm_b200.h — C-ABI of the B200-native GLM / TPA-SCD hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Two levels:
+ *
+ *  (1) Reference-facing, HOST buffers (the drop-in boundary).  These replace
+ *      the reference's device-solve plugin hook:
+ *        Engine(..., chunk_runner=fn) -> fn(sub, dev, cfg)
+ *        (/root/reference/pkg/src/hierglm/engine.py:177-179, 228-233)
+ *      whose default body is damped_solve(sub, dev.gen, cfg.epochs, ...,
+ *      damping=dev.damping) (solver.py:250-305).  glm_ctx_* owns a device
+ *      partition (the matrix resident in HBM, created once like the reference's
+ *      _Device.data, engine.py:113-118); glm_device_solve is one subtask.
+ *
+ *  (2) Device-resident (DEVICE pointers + a cudaStream_t passed as void*):
+ *      the kernels the Python engine drives without host round-trips.
+ *
+ * Status codes (mapped 1:1 onto the reference's exceptions by the host layer):
+ *   GLM_OK                0
+ *   GLM_SOLVER_ERROR      1  -> SolverError      (solver.py:31-32, 160-161, 185-186, 279-280)
+ *   GLM_DIVERGENCE        2  -> SolverDivergence (solver.py:35-38, 289-293)
+ *   GLM_USAGE             3  -> ValueError / UsageError
+ *   GLM_CUDA_ERROR        4  -> RuntimeError (CUDA failure; message via glm_last_error)
+ *
+ * Objective kinds: indices 0..3 are objectives.py:22 KINDS in order; 4..7 are
+ * restated kinds (parity unpinned by the reference).
+ */
+#ifndef GLM_B200_H
+#define GLM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLM_OK 0
+#define GLM_SOLVER_ERROR 1
+#define GLM_DIVERGENCE 2
+#define GLM_USAGE 3
+#define GLM_CUDA_ERROR 4
+
+enum glm_kind {
+    GLM_DUAL_L2_LOGISTIC = 0,     /* objectives.py:5  */
+    GLM_DUAL_L2_SVM = 1,          /* objectives.py:7  */
+    GLM_RIDGE_PRIMAL = 2,         /* objectives.py:8  */
+    GLM_LASSO_PRIMAL = 3,         /* objectives.py:9  */
+    GLM_DUAL_RIDGE = 4,           /* restated */
+    GLM_ELASTIC_NET_PRIMAL = 5,   /* restated */
+    GLM_LOGISTIC_PRIMAL = 6,      /* restated */
+    GLM_SQUARED_HINGE_PRIMAL = 7  /* restated */
+};
+
+enum glm_layout { GLM_CSC = 0, GLM_DENSE = 1 };
+
+enum glm_mode {
+    GLM_MODE_SEQUENTIAL = 0,  /* deterministic fixed-permutation mode: run_pass n_threads=1 (solver.py:202-211) */
+    GLM_MODE_ASYNC = 1        /* TPA-SCD: concurrent coordinate groups, atomic scatter (solver.py:213-239) */
+};
+
+/* Matrix in HBM.  CSC: indptr i64[n_cols+1], rows i32[nnz] (sorted unique per
+ * column), vals f64[nnz]  (data.py:42-62).  DENSE: vals f64[n_rows*n_cols]
+ * column-major (column j at vals + j*n_rows), indptr/rows NULL. */
+typedef struct {
+    int64_t n_rows;
+    int64_t n_cols;
+    int64_t nnz;
+    int32_t layout;
+    int32_t _pad;
+    const int64_t *indptr;
+    const int32_t *rows;
+    const double *vals;
+    const double *sqnorms;   /* f64[n_cols] (col_sqnorms, data.py:98-107) */
+} glm_matrix;
+
+/* One subtask (the LocalSubproblem of solver.py:107-135) on device memory. */
+typedef struct {
+    int32_t kind;
+    int32_t mode;           /* glm_mode */
+    double lam;
+    double l1_ratio;        /* elastic-net rho (kind 5); ignored otherwise */
+    double quad;            /* LocalSubproblem.quad */
+    const double *cnst;     /* device scalar: LocalSubproblem.const */
+    const double *lin;      /* device f64[n_rows] */
+    const double *base;     /* device f64[n_cols] */
+    const double *coord_target; /* device f64[n_cols] per-coordinate y (kind 4) or NULL */
+    int32_t epochs;         /* t_epochs (solver.py:250) */
+    int32_t max_attempts;   /* 0 = run until done (host-synchronous retry loop) */
+    int32_t group_lanes;    /* async: lanes per coordinate (0 = auto) */
+    int32_t max_inflight;   /* async: cap on concurrently processed coordinates
+                               (0 = auto: min(resident groups, n/32)) */
+    int32_t reset_damping;  /* 1: DampingState.reset() before solving (engine.py:251-252) */
+} glm_solve_args;
+
+/* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */
+typedef struct {
+    int32_t status;
+    int32_t epochs_run;
+    int32_t retries;
+    int32_t plateaued;
+    int32_t attempts;       /* scd_epoch calls == permutations consumed */
+    int32_t done;
+    double damping;         /* DampingState.delta after the solve */
+    double initial_value;   /* initial_subproblem_value */
+    double final_value;     /* final_subproblem_value (= DampingState.last_subproblem_value) */
+    uint64_t gen_state;     /* PermutationGenerator.state after the solve */
+} glm_solve_result;
+
+typedef struct glm_solver glm_solver;   /* per-partition scratch + device state */
+typedef struct glm_ctx glm_ctx;         /* host-facing partition: matrix + solver */
+
+/* ---------------------------------------------------------------- misc */
+const char *glm_last_error(void);
+int glm_version(void);
+/* Number of kernels this library has launched (process-wide, monotone). */
+long long glm_launch_count(void);
+int glm_device_count(int *out);
+/* Host-side xorshift64 jump: state after `steps` steps (solver.py:41-46). */
+uint64_t glm_xorshift_jump(uint64_t state, uint64_t steps);
+uint64_t glm_derive_seed(uint64_t base, const uint64_t *idx, int n_idx); /* solver.py:57-61 */
+
+/* ------------------------------------------------ (1) host-facing drop-in */
+/* Copy a host CSC/dense partition into HBM and compute its column norms.
+ * Replaces _Device(...) data placement (engine.py:113-118). */
+int glm_ctx_create(int device, int layout, int64_t n_rows, int64_t n_cols,
+                   const int64_t *indptr, const int32_t *rows, const double *vals,
+                   glm_ctx **out);
+int glm_ctx_destroy(glm_ctx *ctx);
+/* One device subtask with HOST buffers: the semantics of
+ * damped_solve(sub, gen, epochs, n_threads, damping) (solver.py:250-305) where
+ * mode selects sequential (n_threads=1) or asynchronous execution.
+ * gen_state_io  <-> dev.gen.state          (solver.py:70-89)
+ * damping_io    <-> dev.damping.delta      (solver.py:92-104)
+ * values_out    <-  SubtaskResult.epoch_values (capacity `epochs`)
+ * info_out[5]   <-  epochs_run, retries, plateaued, attempts, status
+ * scal_out[2]   <-  initial / final subproblem value */
+int glm_device_solve(glm_ctx *ctx, int kind, double lam, double l1_ratio,
+                     const double *coord_target, const double *lin, double quad,
+                     double cnst, const double *base, uint64_t *gen_state_io,
+                     double *damping_io, int epochs, int mode, double *dalpha_out,
+                     double *dv_out, double *values_out, int32_t *info_out,
+                     double *scal_out);
+/* Fused duality gap over the ctx partition with host buffers
+ * (objectives.duality_gap, objectives.py:223-234): out[0]=f(v)+f*(w),
+ * out[1]=sum g(alpha), out[2]=sum g*(-a^T w), out[3]=f(v). */
+int glm_ctx_gap_terms(glm_ctx *ctx, int kind, double lam, double l1_ratio,
+                      const double *target, const double *coord_target,
+                      const double *alpha, const double *v, double *out);
+
+/* --------------------------------------------- (2) device-resident API */
+int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solver **out);
+int glm_solver_destroy(glm_solver *s);
+/* Set the solver's permutation stream (PermutationGenerator(seed).state) and
+ * damping (DampingState.delta) held in device memory. */
+int glm_solver_set_state(glm_solver *s, uint64_t gen_state, double damping, void *stream);
+/* Asynchronous subtask: all attempts are enqueued on `stream`; outputs are
+ * device arrays.  If args->max_attempts == 0 the call synchronises to run the
+ * retry loop to completion and fills `res`; otherwise it enqueues exactly
+ * max_attempts attempts (skipped on device once done) and `res` may be NULL
+ * (read later with glm_solver_result). */
+int glm_solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *args,
+              double *delta_out, double *dv_out, glm_solve_result *res, void *stream);
+/* Bracket every attempt with CUDA events on the solve stream:
+ * ms_out[0] = permutation kernels, [1] = snapshot + epoch kernel, [2] = value
+ * kernel, summed over the attempts since the last read; *n_out = attempts. */
+int glm_solver_timing(glm_solver *s, int enable);
+int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out);
+/* Copy the device-side solve state to the host (synchronises `stream`).
+ * epoch_values may be NULL; else capacity >= epochs of the last solve. */
+int glm_solver_result(glm_solver *s, glm_solve_result *res, double *epoch_values,
+                      int capacity, void *stream);
+
+/* Permutations (solver.py:77-89, pipeline.py:29-78).  keys/perm are device. */
+int glm_perm_keys(uint64_t state, int64_t n, uint32_t *keys, void *stream);
+int glm_chunk_keys(uint64_t seed, int64_t n, uint32_t *keys, void *stream);
+size_t glm_argsort_temp_bytes(int64_t n);
+/* stable argsort of u32 keys -> int32 perm (np.argsort(kind="stable")) */
+int glm_argsort_u32(const uint32_t *keys, int64_t n, int32_t *perm, void *temp,
+                    size_t temp_bytes, void *stream);
+
+/* Data layer (data.py:98-187, cli.py:146-185).  All device pointers. */
+int glm_col_sqnorms(const glm_matrix *A, double *out, void *stream);
+int glm_matvec(const glm_matrix *A, const double *x, double *out, void *stream);   /* out = A x (atomic scatter) */
+int glm_rmatvec(const glm_matrix *A, const double *w, double *out, void *stream);  /* out = A^T w */
+/* Stable transpose (data.py:155-165): outputs sized n_rows+1 / nnz / nnz. */
+size_t glm_transpose_temp_bytes(int64_t nnz, int64_t n_rows);
+int glm_transpose(const glm_matrix *A, int64_t *indptr_t, int32_t *rows_t, double *vals_t,
+                  void *temp, size_t temp_bytes, void *stream);
+/* select_columns (data.py:132-145): cols i64[k]; glm_select_indptr fills
+ * out_indptr i64[k+1] (device scan), then glm_select_gather copies. */
+size_t glm_select_temp_bytes(int64_t k);
+int glm_select_indptr(const glm_matrix *A, const int64_t *cols, int64_t k,
+                      int64_t *out_indptr, void *temp, size_t temp_bytes, void *stream);
+int glm_select_gather(const glm_matrix *A, const int64_t *cols, int64_t k,
+                      const int64_t *out_indptr, int32_t *out_rows, double *out_vals,
+                      void *stream);
+/* scale_columns (data.py:147-153): vals_out[p] = vals[p] * scales[col(p)] */
+int glm_scale_columns(const glm_matrix *A, const double *scales, double *vals_out,
+                      void *stream);
+/* Validation (data.py:64-84); synchronises `stream`.  GLM_USAGE + message on failure. */
+int glm_validate(const glm_matrix *A, void *stream);
+
+/* Objective / engine glue (objectives.py:129-234, engine.py:131-166, 269-351).
+ * Scalars are device f64 pointers so rounds never leave the device.
+ * `scratch`: device buffer of glm_reduce_scratch_bytes(), zero-filled once,
+ * not shared by concurrently running calls (deterministic block-order sums). */
+size_t glm_reduce_scratch_bytes(void);
+/* grad = f'(v) (grad may be NULL); out_fv[0] = f(v) */
+int glm_fgrad(int kind, double lam, const double *target, const double *v, int64_t d,
+              double *grad, double *out_fv, double *scratch, void *stream);
+/* Inner subproblem (engine.py:148-166) with the outer model (engine.py:242-250):
+ * lin = grad + qo*vbar; cnst_out = (fv/K + grad.vbar + qo/2 |vbar|^2) / L.
+ * vbar may be NULL (= 0). */
+int glm_inner_model(const double *grad, const double *vbar, int64_t d, double qo,
+                    const double *fv, double n_nodes, double n_devices, double *lin,
+                    double *cnst_out, double *scratch, void *stream);
+/* y = a*x + b*y elementwise (fold / apply steps, engine.py:264-266, 302-306) */
+int glm_axpby(int64_t n, double a, const double *x, double b, double *y, void *stream);
+/* Fused gap terms (engine.py:325-351, objectives.py:223-234) over partition A:
+ * out[0] = f(v)+f*(w), out[1] = sum g(alpha), out[2] = sum g*(-a^T w), out[3] = f(v).
+ * w_scratch f64[n_rows]. */
+int glm_gap_terms(const glm_matrix *A, int kind, double lam, double l1_ratio,
+                  const double *target, const double *coord_target, const double *alpha,
+                  const double *v, double *w_scratch, double *out, double *scratch,
+                  void *stream);
+/* out[0] = sum g(alpha) (g_sum, objectives.py:165-173) */
+int glm_gsum(int kind, double lam, double l1_ratio, const double *coord_target,
+             const double *alpha, int64_t n, double *out, double *scratch, void *stream);
+/* Prediction over an example-major matrix X (columns = examples, n_rows <= len(w)):
+ * scores = X^T w (decision_scores, modelio.py:64-75); prob = 0.5(1+tanh(z/2));
+ * out[0] = -sum[y log p + (1-y) log(1-p)] (clip 1e-15), out[1] = #(p>=0.5 == y>0),
+ * out[2] = sum (score - y)^2.  y (raw labels) may be NULL. */
+int glm_predict(const glm_matrix *X, const double *w, const double *y, int classify,
+                double *scores, double *prob, double *out, double *scratch, void *stream);
+/* Batched undamped coordinate steps (coordinate_update, solver.py:152-187)
+ * from (ga, c = quad*|a|^2, t) triples.  GLM_SOLVER_ERROR if any non-finite. */
+int glm_coordinate_steps(int kind, double lam, double l1_ratio, const double *y,
+                         const double *ga, const double *c, const double *t, int64_t n,
+                         double *step, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -363,7 +363,8 @@ def scale_columns(m, scales):
 # ------------------------------------------------------------- engine
 def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed=0,
           rounds=1, sigma=None, sigma_bar=None, strategy="contiguous", rho=1.0, y=None,
-          parallel=False, target_gap=None, time_budget_s=None, record_gap=True):
+          parallel=False, target_gap=None, time_budget_s=None, record_gap=True,
+          record_obj=True, target_rel_gap=None):
     """Engine.train (engine.py:169-417) restated: K nodes x L devices, t2 inner rounds.
 
     Returns dict(objective, gap, alpha, v, rounds). With parallel=True, the
@@ -390,6 +391,10 @@ def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed
     objs, gaps = [], []
 
     def record():
+        if not record_obj:
+            objs.append(np.nan)
+            gaps.append(np.nan)
+            return None
         fv = f_eval(k, lam, target, v)
         obj = fv + g_sum(k, lam, alpha, rho, y)
         gap = None
@@ -401,11 +406,15 @@ def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed
 
     t0 = time.perf_counter()
     gap = record()
+    if target_rel_gap is not None:
+        target_gap = target_rel_gap * abs(objs[0])
     pool = ThreadPoolExecutor(max_workers=K * L) if parallel else None
     done = 0
+    round_s = []
     for _ in range(rounds):
         if target_gap is not None and gap is not None and gap <= target_gap:
             break
+        tr = time.perf_counter()
         grad = f_grad(k, lam, target, v)                   # engine.py:271
         fv = f_eval(k, lam, target, v)
         qo = sig * beta
@@ -443,13 +452,14 @@ def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed
                 alpha[subs[node * L + l][0]] += d_sl[l]
         v += total
         done += 1
+        round_s.append(time.perf_counter() - tr)
         gap = record()
         if time_budget_s is not None and time.perf_counter() - t0 > time_budget_s:
             break
     if pool:
         pool.shutdown()
     return {"objective": np.array(objs), "gap": np.array(gaps), "alpha": alpha, "v": v,
-            "rounds": done}
+            "rounds": done, "round_s": round_s, "wall_s": time.perf_counter() - t0}
 
 
 def train_chunked(m, kind, lam, chunk_size, *, target=None, epochs=1, seed=0, rounds=1,

@@ -1,0 +1,194 @@
+"""Shared-vector reducers: the reference's Reducer duck type over NCCL.
+
+Reference: comm.py:41-114 (canonical_sum, InProcessReducer, participant API:
+allreduce_sum / broadcast / handshake / abort / close) and comm.py:437-444
+(make_reducer). The TCP star/ring reducers (comm.py:117-434) are replaced by
+NCCL over NVLink 5 / NVSwitch through torch.distributed: one process per GPU.
+
+* `NcclReducer(deterministic=False)`: allreduce_sum is one ncclAllReduce
+  (f64, sum) — identical on every rank, summation order chosen by NCCL.
+* `NcclReducer(deterministic=True)`: ncclAllGather + a fold in ascending rank
+  order, bit-identical to canonical_sum (comm.py:41-46).
+Both accept CUDA tensors (device-resident engine) or numpy arrays.
+`make_reducer("gloo", ...)` gives the same semantics on CPU tensors for the
+multi-process tests without a GPU.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+PROTOCOL_VERSION = 1
+
+
+class ReduceError(RuntimeError):
+    pass
+
+
+class ProtocolError(ReduceError):
+    pass
+
+
+def canonical_sum(vectors):
+    """Left-fold sum in ascending rank order (comm.py:41-46)."""
+    out = vectors[0].clone() if isinstance(vectors[0], torch.Tensor) else vectors[0].copy()
+    for vec in vectors[1:]:
+        out += vec
+    return out
+
+
+class InProcessReducer:
+    """Collective sum across `world` threads of one process (comm.py:53-63)."""
+
+    def __init__(self, world):
+        self.world = world
+        self._barrier = threading.Barrier(world)
+        self._slots = [None] * world
+        self._result = None
+
+    def participant(self, rank):
+        return _InProcessParticipant(self, rank)
+
+
+class _InProcessParticipant:
+    topology = "in_process"
+
+    def __init__(self, owner, rank):
+        self.owner = owner
+        self.rank = rank
+
+    def handshake(self):
+        return {"rank": self.rank, "world": self.owner.world, "version": PROTOCOL_VERSION}
+
+    def _wait(self):
+        try:
+            self.owner._barrier.wait()
+        except threading.BrokenBarrierError:
+            raise ReduceError("collective aborted by a peer") from None
+
+    def allreduce_sum(self, vec):
+        owner = self.owner
+        owner._slots[self.rank] = vec
+        self._wait()
+        if self.rank == 0:
+            lengths = {len(s) for s in owner._slots}
+            owner._result = ProtocolError("vector length mismatch") if len(lengths) != 1 \
+                else canonical_sum(owner._slots)
+        self._wait()
+        result = owner._result
+        self._wait()
+        if isinstance(result, Exception):
+            raise result
+        return result.clone() if isinstance(result, torch.Tensor) else result.copy()
+
+    def broadcast(self, vec):
+        owner = self.owner
+        if self.rank == 0:
+            owner._result = vec
+        self._wait()
+        result = owner._result
+        self._wait()
+        return result.clone() if isinstance(result, torch.Tensor) else np.array(result)
+
+    def abort(self):
+        self.owner._barrier.abort()
+
+    def close(self):
+        pass
+
+
+class NcclReducer:
+    """Reducer duck type over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    topology = "nccl"
+
+    def __init__(self, group=None, deterministic=False, device=None):
+        if not dist.is_initialized():
+            raise ReduceError("torch.distributed is not initialised")
+        self.group = group
+        self.deterministic = deterministic
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        self.on_cuda = backend == "nccl"
+        self.device = device if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if self.on_cuda
+            else torch.device("cpu"))
+        self._aborted = False
+
+    def handshake(self):
+        probe = torch.tensor([self.rank, PROTOCOL_VERSION], dtype=torch.float64,
+                             device=self.device)
+        got = [torch.empty_like(probe) for _ in range(self.world)]
+        dist.all_gather(got, probe, group=self.group)
+        ranks = sorted(int(g[0].item()) for g in got)
+        if ranks != list(range(self.world)) or any(int(g[1].item()) != PROTOCOL_VERSION
+                                                   for g in got):
+            raise ProtocolError("handshake mismatch")
+        return {"rank": self.rank, "world": self.world, "version": PROTOCOL_VERSION}
+
+    def _tensor(self, vec):
+        if isinstance(vec, torch.Tensor):
+            return vec.to(self.device, torch.float64).contiguous(), True
+        return torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64)).to(self.device), False
+
+    def allreduce_sum(self, vec, out=None):
+        if self._aborted:
+            raise ReduceError("collective aborted")
+        t, was_tensor = self._tensor(vec)
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=self.device)
+        nmax, nmin = n.clone(), n.clone()
+        if self.world > 1:
+            dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=self.group)
+            dist.all_reduce(nmin, op=dist.ReduceOp.MIN, group=self.group)
+        if int(nmax.item()) != int(nmin.item()):
+            raise ProtocolError("vector length mismatch")
+        if self.deterministic:
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            dist.all_gather(parts, t, group=self.group)
+            res = canonical_sum(parts)      # ascending rank order
+        else:
+            res = t.clone()
+            dist.all_reduce(res, op=dist.ReduceOp.SUM, group=self.group)
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res if was_tensor else res.cpu().numpy()
+
+    def allreduce_inplace(self, t):
+        """Fast path for device-resident engines: sum into `t` (NCCL)."""
+        if self.deterministic:
+            t.copy_(self.allreduce_sum(t))
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def broadcast(self, vec):
+        t, was_tensor = self._tensor(vec)
+        t = t.clone()
+        dist.broadcast(t, src=0 if self.group is None else dist.get_global_rank(self.group, 0),
+                       group=self.group)
+        return t if was_tensor else t.cpu().numpy()
+
+    def barrier(self):
+        dist.barrier(group=self.group)
+
+    def abort(self):
+        self._aborted = True
+
+    def close(self):
+        pass
+
+
+def make_reducer(kind="nccl", rank=None, peers=None, dim=None, deterministic=False):
+    """Factory (comm.py:437-444): 'nccl' | 'gloo' use the initialised process
+    group; 'inproc' returns a single-participant in-process reducer."""
+    if kind in ("nccl", "gloo"):
+        return NcclReducer(deterministic=deterministic)
+    if kind == "inproc":
+        return InProcessReducer(1).participant(0)
+    raise ValueError(f"unknown reducer {kind!r} (TCP reducers are replaced by NCCL)")

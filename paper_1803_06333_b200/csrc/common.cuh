@@ -1,0 +1,226 @@
+// common.cuh — shared device code for the B200 GLM/TPA-SCD kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "glm_b200.h"
+
+namespace glm {
+
+constexpr double BOUNDARY_EPS = 1e-12;          // objectives.py:26
+constexpr double DAMPING_FLOOR = 9.5367431640625e-07;  // 2^-20, solver.py:28
+constexpr double PLATEAU_REL = 1e-12;           // solver.py:247
+constexpr int MAX_EPOCH_VALUES = 256;           // epoch_values kept per solve
+constexpr int NUM_SMS = 148;                    // B200
+
+// Device-resident solver state: the reference's DampingState + the control
+// flow of damped_solve (solver.py:250-305) turned into a state machine that
+// the kernels of one attempt read, so attempts can be enqueued without host
+// round-trips.
+struct SolveState {
+    uint64_t gen_state;       // PermutationGenerator.state at solve start
+    uint64_t gen_next;        // state after the solve (finalize)
+    double damping;           // DampingState.delta
+    double value;             // current accepted G
+    double initial;           // G(0)
+    int32_t epochs_target;
+    int32_t epochs_run;
+    int32_t retries;
+    int32_t plateaued;
+    int32_t attempts;         // scd_epoch calls executed (== permutations consumed)
+    int32_t status;           // GLM_OK / GLM_SOLVER_ERROR / GLM_DIVERGENCE
+    int32_t done;
+    int32_t dc;               // current delta buffer
+    int32_t vw;               // working view buffer
+    int32_t launched;         // attempts enqueued so far (host bookkeeping mirror)
+    uint32_t block_counter;   // last-block-done counter for reductions
+    int32_t _pad;
+    double epoch_values[MAX_EPOCH_VALUES];
+};
+
+__device__ __forceinline__ double ld_cg(const double *p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void red_add(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
+
+// Block reduction of NV doubles (blockDim multiple of 32, <= 1024).
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* >= 32*NV */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) smem[i * 32 + warp] = v[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double x = lane < nw ? smem[i * 32 + lane] : 0.0;
+            v[i] = warp_sum(x);
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- objectives
+__device__ __forceinline__ bool kind_is_dual(int kind) {
+    return kind == GLM_DUAL_L2_LOGISTIC || kind == GLM_DUAL_L2_SVM || kind == GLM_DUAL_RIDGE;
+}
+
+__device__ __forceinline__ double entropy(double a) {   // objectives.py:142-147
+    double t1 = a > 0.0 ? a * log(fmax(a, 1e-320)) : 0.0;
+    double b = 1.0 - a;
+    double t2 = a < 1.0 ? b * log(fmax(b, 1e-320)) : 0.0;
+    return t1 + t2;
+}
+
+__device__ __forceinline__ double softplus(double s) {   // np.logaddexp(0, s)
+    return s > 0.0 ? s + log1p(exp(-s)) : log1p(exp(s));
+}
+
+__device__ __forceinline__ double sigmoid_tanh(double z) {   // modelio.py:78-79
+    return 0.5 * (1.0 + tanh(0.5 * z));
+}
+
+// g_i(a) (objectives.py:150-173; restated kinds 4..7)
+__device__ __forceinline__ double g_one(int kind, double lam, double rho, double y, double a) {
+    switch (kind) {
+    case GLM_DUAL_L2_LOGISTIC: return entropy(a);
+    case GLM_DUAL_L2_SVM: return -a;
+    case GLM_RIDGE_PRIMAL:
+    case GLM_LOGISTIC_PRIMAL:
+    case GLM_SQUARED_HINGE_PRIMAL: return 0.5 * lam * a * a;
+    case GLM_LASSO_PRIMAL: return lam * fabs(a);
+    case GLM_DUAL_RIDGE: return 0.5 * a * a - y * a;
+    case GLM_ELASTIC_NET_PRIMAL: return lam * (rho * fabs(a) + 0.5 * (1.0 - rho) * a * a);
+    }
+    return NAN;
+}
+
+// g_i*(s) (objectives.py:211-220); NAN when no closed form
+__device__ __forceinline__ double g_conj_one(int kind, double lam, double rho, double y, double s) {
+    switch (kind) {
+    case GLM_DUAL_L2_LOGISTIC: return softplus(s);
+    case GLM_DUAL_L2_SVM: return fmax(0.0, s + 1.0);
+    case GLM_RIDGE_PRIMAL:
+    case GLM_LOGISTIC_PRIMAL:
+    case GLM_SQUARED_HINGE_PRIMAL: return s * s / (2.0 * lam);
+    case GLM_DUAL_RIDGE: { double u = s + y; return 0.5 * u * u; }
+    case GLM_ELASTIC_NET_PRIMAL: {
+        if (rho >= 1.0) return NAN;
+        double u = fabs(s) - lam * rho;
+        return u > 0.0 ? u * u / (2.0 * lam * (1.0 - rho)) : 0.0;
+    }
+    }
+    return NAN;
+}
+
+// Undamped 1-D step (coordinate_update, solver.py:152-187) from ga and
+// c = quad*||a||^2.  Returns false on a solver error (non-finite).
+__device__ __forceinline__ bool coord_step(int kind, double lam, double rho, double y, double ga,
+                                           double c, double t, double &step) {
+    if (!isfinite(ga)) return false;
+    switch (kind) {
+    case GLM_RIDGE_PRIMAL:
+    case GLM_LOGISTIC_PRIMAL:
+    case GLM_SQUARED_HINGE_PRIMAL:
+        step = -(ga + lam * t) / (c + lam);
+        return true;
+    case GLM_ELASTIC_NET_PRIMAL:
+        if (rho < 1.0) {
+            double den = c + lam * (1.0 - rho);
+            double z = c * t - ga;
+            double m = fabs(z) - lam * rho;
+            step = copysign(m > 0.0 ? m : 0.0, z) / den - t;
+            return true;
+        }
+        // rho == 1: exactly the lasso path below
+    case GLM_LASSO_PRIMAL: {
+        if (c == 0.0) { step = -t; return true; }
+        double u = t - ga / c, thr = lam / c;
+        double m = fabs(u) - thr;
+        step = copysign(m > 0.0 ? m : 0.0, u) - t;
+        return true;
+    }
+    case GLM_DUAL_L2_SVM: {
+        double tn;
+        if (c == 0.0) tn = ga < 1.0 ? 1.0 : 0.0;
+        else tn = fmin(1.0, fmax(0.0, t + (1.0 - ga) / c));
+        step = tn - t;
+        return true;
+    }
+    case GLM_DUAL_RIDGE:
+        step = -(ga + t - y) / (c + 1.0);
+        return true;
+    case GLM_DUAL_L2_LOGISTIC: {
+        double grad = ga + log(t / (1.0 - t));
+        double curv = c + 1.0 / (t * (1.0 - t));
+        double tn = t - grad / curv;
+        tn = fmin(1.0 - BOUNDARY_EPS, fmax(BOUNDARY_EPS, tn));
+        if (!isfinite(tn)) return false;
+        step = tn - t;
+        return true;
+    }
+    }
+    return false;
+}
+
+// f contributions per row r (objectives.py:129-139, 205-208)
+__device__ __forceinline__ void f_terms(int kind, double lam, double tgt, double v, double &f,
+                                        double &g) {
+    if (kind_is_dual(kind)) { f = v * v / (2.0 * lam); g = v / lam; return; }
+    if (kind == GLM_LOGISTIC_PRIMAL) {
+        f = softplus(-tgt * v);
+        g = -tgt * sigmoid_tanh(-tgt * v);
+        return;
+    }
+    if (kind == GLM_SQUARED_HINGE_PRIMAL) {
+        double m = 1.0 - tgt * v;
+        f = m > 0.0 ? 0.5 * m * m : 0.0;
+        g = m > 0.0 ? -tgt * m : 0.0;
+        return;
+    }
+    double e = v - tgt;
+    f = 0.5 * e * e;
+    g = e;
+}
+
+__device__ __forceinline__ double f_conj_term(int kind, double lam, double tgt, double w) {
+    if (kind_is_dual(kind)) return 0.5 * lam * w * w;
+    if (kind == GLM_LOGISTIC_PRIMAL) return entropy(-w * tgt);
+    if (kind == GLM_SQUARED_HINGE_PRIMAL) { double q = -w * tgt; return 0.5 * q * q - q; }
+    return 0.5 * w * w + w * tgt;
+}
+
+// Host-side count of kernels this library launched (bench.py "gpu_launches").
+void count_launch();
+
+}  // namespace glm
+
+#define GLM_CUDA_TRY(expr)                                                   \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) return glm_set_cuda_error(_e, #expr, __FILE__, __LINE__); \
+    } while (0)
+
+int glm_set_cuda_error(cudaError_t e, const char *what, const char *file, int line);
+int glm_set_error(int code, const char *msg);

@@ -1,0 +1,597 @@
+// scd.cu — the TPA-SCD local solver on B200 (sm_100a).
+//
+// Replaces damped_solve / scd_epoch / run_pass / coordinate_update
+// (solver.py:152-305).  One subtask = begin -> G(0) -> attempts -> finalize,
+// where each attempt is
+//     permutation (prng.cu)  ->  snapshot view  ->  epoch kernel  ->  value+decide
+// and the damping control flow of damped_solve (restore / plateau / halve /
+// divergence, solver.py:272-298) runs in the last block of the value kernel
+// against a device-resident SolveState.  Attempts therefore queue on the
+// stream with no host round-trip; once the state says `done` every later
+// kernel of the subtask exits at its first instruction.
+//
+// Epoch kernels:
+//  * scd_seq   — GLM_MODE_SEQUENTIAL, the deterministic fixed-permutation
+//                mode: one CTA walks the permutation exactly like
+//                run_pass(n_threads=1); the view lives in shared memory when
+//                it fits (d <= 24k), otherwise in global memory.
+//  * scd_async — GLM_MODE_ASYNC (TPA-SCD): a group of G lanes owns one
+//                coordinate j = perm[k]; coalesced loads of the column, a
+//                gather of the shared view through L2 (ld.global.cg),
+//                shuffle reduction, the closed-form / Newton step on lane 0,
+//                and red.global.add.f64 scatter of quad*step*a_j into the view.
+//                Concurrent groups read stale views by design (solver.py:8-13,
+//                SPEC.md:261-262); the damping check discards bad epochs.
+//
+// Memory: delta is double-buffered (every coordinate is visited exactly once
+// per epoch, so the epoch reads delta[dc] and writes delta[dc^1] — accept is a
+// buffer flip, reject costs nothing); the view is snapshotted per attempt
+// (d doubles) and a reject flips the working/snapshot roles.
+// Delta v = B delta is recovered as (view - lin)/quad instead of a second
+// SpMV (the reference recomputes it exactly, solver.py:300); the parity tests
+// bound the difference (tests/test_gpu_solver.py).
+
+#include "solver.cuh"
+
+namespace glm {
+
+struct EpochParams {
+    SolveState *st;
+    int kind;
+    double lam, rho, quad;
+    int64_t m, d;
+    const int64_t *indptr;
+    const int32_t *rows;
+    const double *vals;
+    const double *sq;
+    const double *base;
+    const double *y;
+    double *delta0, *delta1;
+    double *view0, *view1;
+    const int32_t *perm;
+};
+
+__device__ __forceinline__ void flag_error(SolveState *st) {
+    atomicCAS(&st->status, GLM_OK, GLM_SOLVER_ERROR);
+}
+
+// --------------------------------------------------------------- async
+template <int G, bool DENSE>
+__global__ void __launch_bounds__(256) scd_async(EpochParams p) {
+    SolveState *st = p.st;
+    if (st->done) return;
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *__restrict__ dcur = dc ? p.delta1 : p.delta0;
+    double *__restrict__ dnext = dc ? p.delta0 : p.delta1;
+    double *view = st->vw ? p.view1 : p.view0;
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / G, gl = lane % G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int kind = p.kind;
+    for (int64_t kb = warp * GPW; kb < p.m; kb += nwarps * GPW) {
+        const int64_t k = kb + sub;
+        const bool valid = k < p.m;
+        const int j = valid ? __ldg(p.perm + k) : 0;
+        int64_t lo = 0, hi = 0;
+        if (valid) {
+            if (DENSE) {
+                lo = (int64_t)j * p.d;
+                hi = lo + p.d;
+            } else {
+                lo = __ldg(p.indptr + j);
+                hi = __ldg(p.indptr + j + 1);
+            }
+        }
+        double acc = 0.0;
+        for (int64_t q = lo + gl; q < hi; q += G) {
+            const int r = DENSE ? (int)(q - lo) : __ldg(p.rows + q);
+            acc += __ldg(p.vals + q) * ld_cg(view + r);
+        }
+        const double ga = group_sum<G>(acc);
+        double step = 0.0;
+        if (valid && gl == 0) {
+            const double dj = dcur[j];
+            const double t = __ldg(p.base + j) + dj;
+            double raw = 0.0;
+            if (!coord_step(kind, p.lam, p.rho, p.y ? __ldg(p.y + j) : 0.0, ga,
+                            p.quad * __ldg(p.sq + j), t, raw)) {
+                flag_error(st);
+                raw = 0.0;
+            }
+            step = damping * raw;
+            dnext[j] = step != 0.0 ? dj + step : dj;
+        }
+        step = __shfl_sync(0xffffffffu, step, sub * G);
+        if (step != 0.0) {
+            const double f = p.quad * step;
+            for (int64_t q = lo + gl; q < hi; q += G) {
+                const int r = DENSE ? (int)(q - lo) : __ldg(p.rows + q);
+                red_add(view + r, f * __ldg(p.vals + q));
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------- sequential
+// One CTA of BS threads walks the permutation in order (run_pass with
+// n_threads=1, solver.py:202-211).  Deterministic: fixed per-thread strides
+// and a fixed reduction tree.
+template <int BS, bool SMEM, bool DENSE>
+__global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
+    SolveState *st = p.st;
+    if (st->done) return;
+    extern __shared__ double sview[];
+    __shared__ double sred[32];
+    __shared__ double sstep;
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = dc ? p.delta1 : p.delta0;
+    double *dnext = dc ? p.delta0 : p.delta1;
+    double *gview = st->vw ? p.view1 : p.view0;
+    double *V = SMEM ? sview : gview;
+    const int t = threadIdx.x;
+    if (SMEM) {
+        for (int64_t r = t; r < p.d; r += BS) sview[r] = gview[r];
+        __syncthreads();
+    }
+    const int kind = p.kind;
+    for (int64_t k = 0; k < p.m; ++k) {
+        const int j = p.perm[k];
+        int64_t lo, hi;
+        if (DENSE) {
+            lo = (int64_t)j * p.d;
+            hi = lo + p.d;
+        } else {
+            lo = p.indptr[j];
+            hi = p.indptr[j + 1];
+        }
+        double acc = 0.0;
+        for (int64_t q = lo + t; q < hi; q += BS) {
+            const int r = DENSE ? (int)(q - lo) : p.rows[q];
+            acc += p.vals[q] * V[r];
+        }
+        acc = warp_sum(acc);
+        if (BS > 32) {
+            if ((t & 31) == 0) sred[t >> 5] = acc;
+            __syncthreads();
+            if (t < 32) {
+                double x = t < BS / 32 ? sred[t] : 0.0;
+                acc = warp_sum(x);
+            }
+        }
+        if (t == 0) {
+            const double dj = dcur[j];
+            const double tt = p.base[j] + dj;
+            double raw = 0.0;
+            if (!coord_step(kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, acc, p.quad * p.sq[j], tt,
+                            raw)) {
+                flag_error(st);
+                raw = 0.0;
+            }
+            const double step = damping * raw;
+            dnext[j] = step != 0.0 ? dj + step : dj;
+            sstep = step;
+        }
+        if (BS > 32) __syncthreads(); else __syncwarp();
+        const double step = sstep;
+        if (step != 0.0) {
+            const double f = p.quad * step;
+            for (int64_t q = lo + t; q < hi; q += BS) {
+                const int r = DENSE ? (int)(q - lo) : p.rows[q];
+                V[r] += f * p.vals[q];
+            }
+        }
+        if (BS > 32) __syncthreads(); else __syncwarp();
+    }
+    if (SMEM) {
+        for (int64_t r = t; r < p.d; r += BS) gview[r] = sview[r];
+    }
+}
+
+// ------------------------------------------------------- value + decide
+struct ValueParams {
+    SolveState *st;
+    int mode;   // 0: initial G(0); 1: after an attempt
+    int kind;
+    double lam, rho, quad;
+    const double *cnst;
+    int64_t m, d;
+    const double *lin, *base, *y;
+    double *delta0, *delta1;
+    double *view0, *view1;
+    double *partials;
+};
+
+// G(delta) = const + lin.w + quad/2 |w|^2 + sum g(base + delta) with
+// quad*w = view - lin, i.e. (lin.u + u.u/2)/quad for u = view - lin
+// (LocalSubproblem.value_given_w, solver.py:132-135).
+__global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
+    SolveState *st = p.st;
+    if (st->done) return;
+    __shared__ double sm[96];
+    __shared__ int s_last;
+    const double *dn = p.mode ? (st->dc ? p.delta0 : p.delta1) : nullptr;
+    const double *V = st->vw ? p.view1 : p.view0;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    if (p.mode) {
+        for (int64_t r = tid; r < p.d; r += nth) {
+            const double v = V[r], l = p.lin[r];
+            if (!isfinite(v)) acc[2] += 1.0;
+            const double u = v - l;
+            acc[0] += l * u + 0.5 * u * u;
+        }
+    }
+    for (int64_t j = tid; j < p.m; j += nth) {
+        const double tt = p.base[j] + (dn ? dn[j] : 0.0);
+        acc[1] += g_one(p.kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, tt);
+    }
+    block_sum<3>(acc, sm);
+    if (threadIdx.x == 0) {
+        p.partials[blockIdx.x * 3 + 0] = acc[0];
+        p.partials[blockIdx.x * 3 + 1] = acc[1];
+        p.partials[blockIdx.x * 3 + 2] = acc[2];
+        __threadfence();
+        const unsigned ticket = atomicAdd(&st->block_counter, 1u);
+        s_last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double tot[3] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        tot[0] += __ldcg(p.partials + b * 3 + 0);
+        tot[1] += __ldcg(p.partials + b * 3 + 1);
+        tot[2] += __ldcg(p.partials + b * 3 + 2);
+    }
+    block_sum<3>(tot, sm);
+    if (threadIdx.x != 0) return;
+    st->block_counter = 0;
+    const double G = *p.cnst + (p.mode ? tot[0] / p.quad : 0.0) + tot[1];
+    if (!p.mode) {
+        st->value = G;
+        st->initial = G;
+        return;
+    }
+    // damped_solve control flow (solver.py:272-298)
+    st->attempts += 1;
+    if (tot[2] > 0.0) {            // solver.py:279-280
+        st->status = GLM_SOLVER_ERROR;
+        st->done = 1;
+        return;
+    }
+    if (st->status != GLM_OK) {    // coordinate-level error (solver.py:160-161, 185-186)
+        st->done = 1;
+        return;
+    }
+    const double value = st->value;
+    if (G > value) {
+        st->vw ^= 1;               // restore the snapshot view; delta[dc] untouched
+        if (G - value <= PLATEAU_REL * (1.0 + fabs(value))) {
+            st->plateaued = 1;
+            st->done = 1;
+            return;
+        }
+        st->retries += 1;
+        st->damping *= 0.5;
+        if (st->damping < DAMPING_FLOOR) {
+            st->status = GLM_DIVERGENCE;
+            st->done = 1;
+        }
+        return;
+    }
+    st->value = G;
+    st->dc ^= 1;
+    if (st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
+    st->epochs_run += 1;
+    if (st->epochs_run >= st->epochs_target) st->done = 1;
+}
+
+// ---------------------------------------------------------- begin / end
+__global__ void begin_kernel(SolveState *st, double *delta0, double *view0, const double *lin,
+                             int64_t m, int64_t d, int epochs, int reset_damping) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = tid; j < m; j += nth) delta0[j] = 0.0;
+    for (int64_t r = tid; r < d; r += nth) view0[r] = lin[r];
+    if (tid == 0) {
+        st->gen_state = st->gen_next;
+        if (reset_damping) st->damping = 1.0;
+        st->epochs_target = epochs;
+        st->epochs_run = 0;
+        st->retries = 0;
+        st->plateaued = 0;
+        st->attempts = 0;
+        st->status = GLM_OK;
+        st->done = 0;
+        st->dc = 0;
+        st->vw = 0;
+        st->block_counter = 0;
+    }
+}
+
+__global__ void snapshot_kernel(const SolveState *st, double *view0, double *view1, int64_t d) {
+    if (st->done) return;
+    const double *src = st->vw ? view1 : view0;
+    double *dst = st->vw ? view0 : view1;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = tid; r < d; r += nth) dst[r] = src[r];
+}
+
+__global__ void finalize_kernel(SolveState *st, const double *delta0, const double *delta1,
+                                const double *view0, const double *view1, const double *lin,
+                                double quad, int64_t m, int64_t d, double *delta_out,
+                                double *dv_out) {
+    const double *dl = st->dc ? delta1 : delta0;
+    const double *V = st->vw ? view1 : view0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    if (delta_out)
+        for (int64_t j = tid; j < m; j += nth) delta_out[j] = dl[j];
+    if (dv_out)
+        for (int64_t r = tid; r < d; r += nth) dv_out[r] = (V[r] - lin[r]) / quad;
+    if (tid == 0) st->gen_next = dev_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
+}
+
+__global__ void empty_solve_kernel(SolveState *st) {
+    for (int i = 0; i < st->epochs_target && i < MAX_EPOCH_VALUES; ++i)
+        st->epoch_values[i] = st->value;
+    st->epochs_run = st->epochs_target;
+    st->done = 1;
+}
+
+__global__ void set_state_kernel(SolveState *st, uint64_t gen, double damping) {
+    st->gen_next = gen;
+    st->damping = damping;
+    st->block_counter = 0;
+    st->done = 1;
+}
+
+// ------------------------------------------------------------- launchers
+static int grid_stride_blocks(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 8 * NUM_SMS) b = 8 * NUM_SMS;
+    return (int)b;
+}
+
+template <int G, bool DENSE>
+static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                                   scd_async<G, DENSE>, 256, 0));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    // Staleness control: at most max_inflight coordinates in flight (default
+    // n/32, i.e. ~3% of the partition) — the GPU analogue of the reference's
+    // thread count (solver.py:213-239).  Large partitions fill the GPU.
+    int64_t groups = max_inflight > 0 ? max_inflight : (p.m + 31) / 32;
+    if (groups > p.m) groups = p.m;
+    if (groups < 32 / G) groups = 32 / G;
+    int64_t need_blocks = (groups * G + 255) / 256;
+    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
+    int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
+    count_launch();
+    scd_async<G, DENSE><<<grid, 256, 0, s>>>(p);
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+template <bool DENSE>
+static int launch_async(const EpochParams &p, int lanes, int max_inflight, cudaStream_t s) {
+    switch (lanes) {
+    case 4: return launch_async_t<4, DENSE>(p, max_inflight, s);
+    case 8: return launch_async_t<8, DENSE>(p, max_inflight, s);
+    case 16: return launch_async_t<16, DENSE>(p, max_inflight, s);
+    default: return launch_async_t<32, DENSE>(p, max_inflight, s);
+    }
+}
+
+constexpr int64_t SMEM_VIEW_MAX = 24 * 1024;   // doubles (192 KB)
+
+template <int BS, bool DENSE>
+static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
+    if (p.d <= SMEM_VIEW_MAX) {
+        size_t bytes = sizeof(double) * (size_t)(p.d > 0 ? p.d : 1);
+        GLM_CUDA_TRY(cudaFuncSetAttribute(scd_seq<BS, true, DENSE>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(SMEM_VIEW_MAX * sizeof(double))));
+        count_launch();
+        scd_seq<BS, true, DENSE><<<1, BS, bytes, s>>>(p);
+    } else {
+        count_launch();
+        scd_seq<BS, false, DENSE><<<1, BS, 0, s>>>(p);
+    }
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+static int auto_lanes(double avg_nnz) {
+    if (avg_nnz <= 12) return 4;
+    if (avg_nnz <= 24) return 8;
+    if (avg_nnz <= 64) return 16;
+    return 32;
+}
+
+int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream) {
+    count_launch();
+    set_state_kernel<<<1, 1, 0, stream>>>(s->st, gen_state ? gen_state : 0x9E3779B97F4A7C15ULL,
+                                          damping);
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int cap,
+                cudaStream_t stream) {
+    GLM_CUDA_TRY(cudaMemcpyAsync(s->st_host, s->st, sizeof(SolveState), cudaMemcpyDeviceToHost,
+                                 stream));
+    GLM_CUDA_TRY(cudaStreamSynchronize(stream));
+    const SolveState &h = *s->st_host;
+    if (res) {
+        res->status = h.status;
+        res->epochs_run = h.epochs_run;
+        res->retries = h.retries;
+        res->plateaued = h.plateaued;
+        res->attempts = h.attempts;
+        res->done = h.done;
+        res->damping = h.damping;
+        res->initial_value = h.initial;
+        res->final_value = h.value;
+        res->gen_state = h.gen_next;
+    }
+    if (epoch_values) {
+        int n = h.epochs_run < cap ? h.epochs_run : cap;
+        n = n < MAX_EPOCH_VALUES ? n : MAX_EPOCH_VALUES;
+        for (int i = 0; i < n; ++i) epoch_values[i] = h.epoch_values[i];
+    }
+    return GLM_OK;
+}
+
+int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *delta_out,
+          double *dv_out, glm_solve_result *res, cudaStream_t stream) {
+    if (!A || !a) return glm_set_error(GLM_USAGE, "null matrix or args");
+    if (a->epochs < 1) return glm_set_error(GLM_USAGE, "t_epochs must be >= 1");
+    const int64_t m = A->n_cols, d = A->n_rows;
+    if (m > s->max_coords || d > s->max_rows)
+        return glm_set_error(GLM_USAGE, "partition larger than the solver was created for");
+    if (m >= (1LL << 31)) return glm_set_error(GLM_USAGE, "partition exceeds 2^31 coordinates");
+    if (a->kind < 0 || a->kind > GLM_SQUARED_HINGE_PRIMAL)
+        return glm_set_error(GLM_USAGE, "unknown objective kind");
+    if (!(a->quad > 0.0)) return glm_set_error(GLM_USAGE, "quad must be positive");
+    if (a->kind == GLM_DUAL_RIDGE && !a->coord_target)
+        return glm_set_error(GLM_USAGE, "dual_ridge needs per-coordinate targets");
+    int rc = ensure_device_tables();
+    if (rc) return rc;
+    const bool dense = A->layout == GLM_DENSE;
+
+    EpochParams ep;
+    ep.st = s->st;
+    ep.kind = a->kind;
+    ep.lam = a->lam;
+    ep.rho = a->l1_ratio;
+    ep.quad = a->quad;
+    ep.m = m;
+    ep.d = d;
+    ep.indptr = A->indptr;
+    ep.rows = A->rows;
+    ep.vals = A->vals;
+    ep.sq = A->sqnorms;
+    ep.base = a->base;
+    ep.y = a->coord_target;
+    ep.delta0 = s->delta[0];
+    ep.delta1 = s->delta[1];
+    ep.view0 = s->view[0];
+    ep.view1 = s->view[1];
+    ep.perm = s->perm;
+
+    ValueParams vp;
+    vp.st = s->st;
+    vp.kind = a->kind;
+    vp.lam = a->lam;
+    vp.rho = a->l1_ratio;
+    vp.quad = a->quad;
+    vp.cnst = a->cnst;
+    vp.m = m;
+    vp.d = d;
+    vp.lin = a->lin;
+    vp.base = a->base;
+    vp.y = a->coord_target;
+    vp.delta0 = s->delta[0];
+    vp.delta1 = s->delta[1];
+    vp.view0 = s->view[0];
+    vp.view1 = s->view[1];
+    vp.partials = s->partials;
+
+    const double avg = dense ? (double)d : (m > 0 ? (double)A->nnz / (double)m : 0.0);
+    const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg);
+    const int seq_bs = avg <= 96.0 ? 32 : 256;
+
+    count_launch();
+    begin_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
+        s->st, s->delta[0], s->view[0], a->lin, m, d, a->epochs, a->reset_damping);
+    vp.mode = 0;
+    count_launch();
+    value_kernel<<<VALUE_BLOCKS, VALUE_THREADS, 0, stream>>>(vp);
+    GLM_CUDA_TRY(cudaGetLastError());
+    vp.mode = 1;
+
+    const PermScratch ps = carve_perm_scratch(s->perm_mem, s->max_coords, m);
+    int launched = 0;
+    auto attempt = [&]() -> int {
+        // optional CUDA-event bracket: [perm | snapshot+epoch | value]
+        std::array<cudaEvent_t, 4> ev{};
+        if (s->timing) {
+            if (!s->event_pool.empty()) {
+                ev = s->event_pool.back();
+                s->event_pool.pop_back();
+            } else {
+                for (int i = 0; i < 4; ++i) GLM_CUDA_TRY(cudaEventCreate(&ev[i]));
+            }
+            GLM_CUDA_TRY(cudaEventRecord(ev[0], stream));
+        }
+        int r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, s->perm, ps, stream);
+        if (r) return r;
+        if (s->timing) GLM_CUDA_TRY(cudaEventRecord(ev[1], stream));
+        count_launch();
+        snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1], d);
+        count_launch();
+        if (a->mode == GLM_MODE_SEQUENTIAL) {
+            if (dense) r = seq_bs == 32 ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
+            else r = seq_bs == 32 ? launch_seq_t<32, false>(ep, stream) : launch_seq_t<256, false>(ep, stream);
+        } else {
+            r = dense ? launch_async<true>(ep, lanes, a->max_inflight, stream)
+                      : launch_async<false>(ep, lanes, a->max_inflight, stream);
+        }
+        if (r) return r;
+        if (s->timing) GLM_CUDA_TRY(cudaEventRecord(ev[2], stream));
+        count_launch();
+        value_kernel<<<VALUE_BLOCKS, VALUE_THREADS, 0, stream>>>(vp);
+        GLM_CUDA_TRY(cudaGetLastError());
+        if (s->timing) {
+            GLM_CUDA_TRY(cudaEventRecord(ev[3], stream));
+            s->events.push_back(ev);
+        }
+        ++launched;
+        return GLM_OK;
+    };
+
+    if (m > 0) {
+        if (a->max_attempts > 0) {
+            for (int i = 0; i < a->max_attempts; ++i)
+                if ((rc = attempt())) return rc;
+        } else {
+            int batch = a->epochs;
+            for (;;) {
+                for (int i = 0; i < batch; ++i)
+                    if ((rc = attempt())) return rc;
+                glm_solve_result r;
+                if ((rc = read_result(s, &r, nullptr, 0, stream))) return rc;
+                if (r.done) break;
+                batch = a->epochs - r.epochs_run;
+                if (batch < 1) batch = 1;
+            }
+        }
+    } else {
+        // no coordinates: the reference still runs `epochs` empty passes whose
+        // value never changes (permute(0) consumes no keys, solver.py:86-88)
+        count_launch();
+        empty_solve_kernel<<<1, 1, 0, stream>>>(s->st);
+    }
+    count_launch();
+    finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
+        s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
+        delta_out, dv_out);
+    GLM_CUDA_TRY(cudaGetLastError());
+    s->last_epochs = a->epochs;
+    s->last_m = m;
+    if (res) return read_result(s, res, nullptr, 0, stream);
+    return GLM_OK;
+}
+
+}  // namespace glm

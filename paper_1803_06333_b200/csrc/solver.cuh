@@ -1,0 +1,39 @@
+// solver.cuh — solver object and kernel-launch entry points shared by the
+// C-ABI translation units.
+#pragma once
+#include "common.cuh"
+#include "prng.cuh"
+
+#include <array>
+#include <vector>
+
+struct glm_solver {
+    int device = 0;
+    int64_t max_coords = 0, max_rows = 0;
+    glm::SolveState *st = nullptr;        // device
+    glm::SolveState *st_host = nullptr;   // pinned mirror
+    double *delta[2] = {nullptr, nullptr};
+    double *view[2] = {nullptr, nullptr};
+    int32_t *perm = nullptr;
+    void *perm_mem = nullptr;
+    double *partials = nullptr;           // value-kernel block partials
+    double *scratch = nullptr;            // generic reduction scratch
+    int timing = 0;                       // record per-attempt CUDA events
+    std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
+    int last_epochs = 0;
+    int64_t last_m = 0;
+};
+
+namespace glm {
+
+constexpr int VALUE_BLOCKS = 2 * NUM_SMS;   // fixed grid => deterministic sums
+constexpr int VALUE_THREADS = 256;
+constexpr size_t REDUCE_SCRATCH_BYTES = 64 * 1024;
+
+int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *delta_out,
+          double *dv_out, glm_solve_result *res, cudaStream_t stream);
+int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int cap,
+                cudaStream_t stream);
+int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
+
+}  // namespace glm

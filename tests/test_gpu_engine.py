@@ -1,0 +1,130 @@
+"""GPU parity of the device-resident CoCoA engine vs the reference's traces
+(tests/golden/engine.npz) and the reference's engine-level properties."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_1803_06333_b200 as g  # noqa: E402
+from paper_1803_06333_b200.objectives import KINDS  # noqa: E402
+
+
+def _case(z, c):
+    p = f"c{c}_"
+    m = g.SparseColumnMatrix(int(z[p + "n_rows"]), z[p + "indptr"], z[p + "rows"],
+                             z[p + "vals"], validate=False)
+    kind = KINDS[int(z[p + "kind"])]
+    tgt = z[p + "target"]
+    if kind.startswith("dual_"):
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]), m.n_cols, m.n_rows)
+    else:
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]), m.n_rows, m.n_cols, target=tgt)
+    K, L, t2, ep, R, cs = (int(x) for x in z[p + "cfg"])
+    strat = "balanced-by-nnz" if int(z[p + "balanced"]) else "contiguous"
+    cfg = g.HierarchyConfig(nodes=K, devices=L, t1=R, t2=t2, seed=cs, epochs=ep,
+                            partition_strategy=strat)
+    return m, spec, cfg, p
+
+
+def test_engine_traces_match_reference(golden):
+    z = golden("engine")
+    for c in range(int(z["n_cases"])):
+        m, spec, cfg, p = _case(z, c)
+        res = g.train(m, spec, cfg, g.StoppingCriteria(max_rounds=cfg.t1))
+        np.testing.assert_allclose(res.trace.objectives(), z[p + "objective"], rtol=1e-10,
+                                   err_msg=f"case {c}")
+        gaps = np.array([np.nan if r.gap is None else r.gap for r in res.trace.rows])
+        np.testing.assert_allclose(gaps, z[p + "gap"], rtol=1e-6, atol=1e-8,
+                                   err_msg=f"case {c}")
+        np.testing.assert_allclose(res.model.alpha, z[p + "alpha"], atol=1e-7)
+        np.testing.assert_allclose(res.v, z[p + "v"], atol=1e-7)
+
+
+def test_flat_equivalence_per_round(golden):
+    """Nested (K=2, L=2, t2=1) == flat K=4 within 1e-12 (test_acceptance.py:41-61)."""
+    z = golden("engine")
+    m, spec, _, _ = _case(z, 0)
+    nested = g.Engine(m, spec, g.HierarchyConfig(nodes=2, devices=2, t1=8, t2=1, sigma=2,
+                                                 sigma_bar=2, seed=13, epochs=2))
+    flat = g.Engine(m, spec, g.HierarchyConfig(nodes=4, devices=1, t1=8, t2=1, sigma=4,
+                                               sigma_bar=1, seed=13, epochs=2))
+    for _ in range(8):
+        nested.outer_round()
+        flat.outer_round()
+        assert np.max(np.abs(nested.alpha - flat.alpha)) < 1e-12
+        assert np.max(np.abs(nested.v - flat.v)) < 1e-12
+
+
+def test_v_consistency_every_round(golden):
+    z = golden("engine")
+    m, spec, _, _ = _case(z, 4)   # dual svm
+    eng = g.Engine(m, spec, g.HierarchyConfig(nodes=2, devices=2, t1=5, t2=2, seed=1))
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    for _ in range(5):
+        eng.outer_round()
+        rec = oracle.matvec(om, eng.alpha)
+        assert np.max(np.abs(eng.v - rec)) < 1e-9 * max(1.0, np.max(np.abs(eng.v)))
+
+
+def test_bit_reproducible(golden):
+    z = golden("engine")
+    m, spec, _, _ = _case(z, 2)
+    runs = []
+    for _ in range(2):
+        runs.append(g.train(m, spec, g.HierarchyConfig(nodes=2, devices=2, t1=4, t2=2, seed=9),
+                            g.StoppingCriteria(max_rounds=4)))
+    np.testing.assert_array_equal(runs[0].model.alpha, runs[1].model.alpha)
+    np.testing.assert_array_equal(runs[0].v, runs[1].v)
+    assert runs[0].trace.objectives().tolist() == runs[1].trace.objectives().tolist()
+
+
+def test_ridge_1x1_one_round():
+    m = g.SparseColumnMatrix(1, [0, 1], [0], [1.0])
+    spec = g.ObjectiveSpec("ridge_primal", 1.0, 1, 1, target=np.array([1.0]))
+    res = g.train(m, spec, g.HierarchyConfig(t1=1, epochs=1), g.StoppingCriteria(max_rounds=1))
+    assert res.trace.rows[-1].objective == pytest.approx(0.25, abs=1e-12)
+    assert res.model.alpha[0] == pytest.approx(0.5, abs=1e-12)
+
+
+def test_stopping_already_met(golden):
+    z = golden("engine")
+    m, spec, _, _ = _case(z, 3)
+    res = g.train(m, spec, g.HierarchyConfig(t1=5), g.StoppingCriteria(max_rounds=5,
+                                                                      target_gap=1e9))
+    assert res.rounds == 0 and res.stop_reason == "target_met"
+
+
+def _c2_like(n, d, k, seed):
+    """Label-folded sparse instance with the C2 shape ratios (k nnz per example)."""
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.integers(0, d - k + 1, size=(n, k)), axis=1) + np.arange(k)
+    vals = rng.standard_normal((n, k))
+    vals /= np.linalg.norm(vals, axis=1, keepdims=True)
+    w = rng.standard_normal(d)
+    score = (vals * w[rows]).sum(axis=1) + 0.3 * rng.standard_normal(n)
+    y = np.where(score >= 0, 1.0, -1.0)
+    return g.SparseColumnMatrix(d, np.arange(0, n * k + 1, k), rows.reshape(-1).astype(np.int32),
+                                (vals * y[:, None]).reshape(-1), labels=y, validate=False)
+
+
+def test_async_engine_reaches_gap_target():
+    """North-star async contract: async TPA-SCD reaches the deterministic
+    (sequential) run's duality-gap target within +-10% of its epochs, on an
+    instance with the C2 shape ratios (40 nnz/example, d = n/10)."""
+    m = _c2_like(200_000, 20_000, 40, 5)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
+    rounds = {}
+    for mode in ("sequential", "async"):
+        eng = g.Engine(m, spec, g.HierarchyConfig(t1=80, seed=3, epochs=1), mode=mode)
+        obj0, _ = eng.objective_and_gap()
+        res = eng.train(g.StoppingCriteria(max_rounds=80, target_gap=1e-6 * abs(obj0)))
+        assert res.stop_reason == "target_met", (mode, res.trace.rows[-1])
+        rounds[mode] = res.rounds
+    print("epochs to target", rounds)
+    assert abs(rounds["async"] - rounds["sequential"]) <= max(1, 0.1 * rounds["sequential"])

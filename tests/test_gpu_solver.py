@@ -1,0 +1,252 @@
+"""GPU parity: permutation stream, coordinate steps and damped_solve vs the
+reference's golden vectors and the CPU oracle (which the golden vectors pin)."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_1803_06333_b200 as g  # noqa: E402
+from paper_1803_06333_b200 import _lib  # noqa: E402
+from paper_1803_06333_b200.objectives import KINDS  # noqa: E402
+
+
+def _spec(kind, m, target=None):
+    k = KINDS[kind] if isinstance(kind, (int, np.integer)) else kind
+    tgt = target if (target is not None and len(target)) else None
+    if k.startswith("dual_") and k != "dual_ridge":
+        return g.ObjectiveSpec(k, 1.0, m.n_cols, m.n_rows)
+    return g.ObjectiveSpec(k, 1.0, m.n_rows, m.n_cols, target=tgt)
+
+
+def _mat(z, p):
+    return g.SparseColumnMatrix(int(z[p + "n_rows"]), z[p + "indptr"], z[p + "rows"],
+                                z[p + "vals"], validate=False)
+
+
+# ----------------------------------------------------------------- PRNG
+def test_permutation_stream_bit_exact(golden):
+    z = golden("prng")
+    for c, (seed, n) in enumerate(z["perm_cases"]):
+        gen = g.PermutationGenerator(int(seed))
+        np.testing.assert_array_equal(g.PermutationGenerator(int(seed)).keys(int(n)),
+                                      z[f"perm{c}_keys"])
+        p1 = gen.permute(int(n))
+        s1 = gen.state
+        p2 = gen.permute(int(n))
+        np.testing.assert_array_equal(p1, z[f"perm{c}_p1"])
+        np.testing.assert_array_equal(p2, z[f"perm{c}_p2"])
+        assert [s1, gen.state] == [int(x) for x in z[f"perm{c}_states"][1:]]
+
+
+def test_permutation_large_vs_oracle():
+    for seed, n in [(5, 1), (7, 4095), (11, 131_073), (13, 1_000_003)]:
+        gen = g.PermutationGenerator(seed)
+        got = gen.permute(n)
+        want, st = oracle.permute(seed, n)
+        np.testing.assert_array_equal(got, want)
+        assert gen.state == st
+
+
+def test_chunk_keys_bit_exact(golden):
+    z = golden("prng")
+    from paper_1803_06333_b200 import pipeline
+    for c, (seed, n) in enumerate(z["gk_cases"]):
+        np.testing.assert_array_equal(pipeline.generate_keys(int(seed), int(n)), z[f"gk{c}"])
+        np.testing.assert_array_equal(pipeline.keys_to_permutation(z[f"gk{c}"]),
+                                      z[f"gk{c}_perm"])
+    big = pipeline.generate_keys(99, 300_001)
+    np.testing.assert_array_equal(big, oracle.generate_keys(99, 300_001))
+
+
+def test_argsort_adversarial_ties():
+    keys = np.zeros(5000, dtype=np.uint32)
+    keys[::7] = 3
+    from paper_1803_06333_b200.solver import argsort_u32_device
+    got = argsort_u32_device(torch.from_numpy(keys).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(got, np.argsort(keys, kind="stable"))
+
+
+# ------------------------------------------------------- coordinate steps
+def test_coordinate_update_kats(golden):
+    t = golden("coord")["table"]
+    for row in t[::3]:
+        kind, nnz = int(row[0]), int(row[1])
+        rows = row[2:6].astype(np.int32)[:nnz]
+        vals = row[6:10][:nnz]
+        view = row[10:14]
+        sq, tt, quad, lam, ga, step = row[14:20]
+        spec = g.ObjectiveSpec(KINDS[kind], lam, 4, 4, target=np.zeros(4))
+        got = g.coordinate_update(spec, rows, vals, sq, tt, view, quad)
+        assert got == pytest.approx(step, rel=1e-12, abs=1e-14)
+
+
+def test_ridge_1x1_one_shot():
+    m = g.SparseColumnMatrix(1, [0, 1], [0], [1.0])
+    spec = g.ObjectiveSpec("ridge_primal", 1.0, 1, 1, target=np.array([1.0]))
+    step = g.coordinate_update(spec, *m.col(0), 1.0, 0.0, np.array([-1.0]), 1.0)
+    assert step == pytest.approx(0.5, abs=1e-15)
+
+
+# -------------------------------------------------------------- solves
+def test_damped_solve_sequential_matches_reference(golden):
+    z = golden("solve")
+    for c in range(int(z["n_cases"])):
+        p = f"c{c}_"
+        m = _mat(z, p)
+        tgt = z[p + "target"]
+        kind = KINDS[int(z[p + "kind"])]
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]),
+                               m.n_cols if kind.startswith("dual_") else m.n_rows,
+                               m.n_rows if kind.startswith("dual_") else m.n_cols,
+                               target=tgt if len(tgt) else None)
+        sub = g.LocalSubproblem(spec=spec, lin=z[p + "lin"], quad=float(z[p + "quad"]),
+                                const=float(z[p + "const"]), base=z[p + "base"], data=m,
+                                col_ids=np.arange(m.n_cols))
+        gen = g.PermutationGenerator(int(z[p + "gen_seed"]))
+        st = g.DampingState()
+        res = g.damped_solve(sub, gen, int(z[p + "epochs"]), n_threads=1, damping=st)
+        assert res.epochs_run == int(z[p + "epochs_run"])
+        assert res.retries == int(z[p + "retries"])
+        assert gen.state == int(z[p + "gen_state"])
+        assert st.delta == float(z[p + "damping"])
+        np.testing.assert_allclose(res.epoch_values, z[p + "values"], rtol=1e-11)
+        assert res.initial_subproblem_value == pytest.approx(float(z[p + "initial"]), rel=1e-12)
+        np.testing.assert_allclose(res.delta_alpha, z[p + "delta"], atol=1e-9)
+        np.testing.assert_allclose(res.delta_v, z[p + "dv"], atol=1e-9)
+        # Delta v = B delta within the reference's own bound (test_solver.py:160-169)
+        dv_exact = oracle.matvec(oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals),
+                                 res.delta_alpha)
+        assert np.max(np.abs(res.delta_v - dv_exact)) < 1e-9 * max(1.0, np.max(np.abs(dv_exact)))
+
+
+def _dual_instance(kind, n, d, nnz, lam, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.empty(n * nnz, np.int32)
+    for j in range(n):
+        rows[j * nnz:(j + 1) * nnz] = np.sort(rng.choice(d, nnz, replace=False))
+    vals = rng.standard_normal(n * nnz)
+    vals = (vals.reshape(n, nnz) / np.linalg.norm(vals.reshape(n, nnz), axis=1,
+                                                  keepdims=True)).reshape(-1)
+    ip = np.arange(0, n * nnz + 1, nnz, dtype=np.int64)
+    y = np.where(rng.standard_normal(n) >= 0, 1.0, -1.0)
+    vals = vals * np.repeat(y, nnz)
+    return g.SparseColumnMatrix(d, ip, rows, vals, validate=False)
+
+
+@pytest.mark.parametrize("kind", ["dual_l2_logistic", "dual_l2_svm"])
+def test_sequential_solve_vs_oracle_medium(kind):
+    m = _dual_instance(kind, 20_000, 2_000, 12, 1.0, 3)
+    spec = g.ObjectiveSpec(kind, 1.0, m.n_cols, m.n_rows)
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    alpha = spec.init_alpha()
+    v = oracle.matvec(om, alpha)
+    lin = oracle.f_grad(KINDS.index(kind), 1.0, None, v)
+    fv = oracle.f_eval(KINDS.index(kind), 1.0, None, v)
+    sub = g.LocalSubproblem(spec=spec, lin=lin, quad=2.0, const=fv, base=alpha, data=m,
+                            col_ids=np.arange(m.n_cols))
+    gen = g.PermutationGenerator(77)
+    res = g.damped_solve(sub, gen, 3)
+    want = oracle.damped_solve(KINDS.index(kind), 1.0, om, lin, 2.0, fv, alpha, 77, 3)
+    assert res.epochs_run == want["epochs_run"] and gen.state == want["gen_state"]
+    np.testing.assert_allclose(res.epoch_values, want["values"], rtol=1e-10)
+    assert abs(res.final_subproblem_value - want["final"]) <= 1e-6 * abs(want["final"])
+    np.testing.assert_allclose(res.delta_alpha, want["delta"], atol=1e-6)
+
+
+def test_async_solve_monotone_and_consistent():
+    m = _dual_instance("dual_l2_logistic", 200_000, 20_000, 16, 1.0, 4)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 0.5, m.n_cols, m.n_rows)
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    alpha = spec.init_alpha()
+    v = oracle.matvec(om, alpha)
+    lin = oracle.f_grad(0, 0.5, None, v)
+    fv = oracle.f_eval(0, 0.5, None, v)
+    sub = g.LocalSubproblem(spec=spec, lin=lin, quad=2.0, const=fv, base=alpha, data=m,
+                            col_ids=np.arange(m.n_cols))
+    res = g.damped_solve(sub, g.PermutationGenerator(9), 4, n_threads=8)
+    vals = [res.initial_subproblem_value] + res.epoch_values
+    assert all(b <= a for a, b in zip(vals, vals[1:]))
+    assert res.final_subproblem_value < res.initial_subproblem_value
+    total = alpha + res.delta_alpha
+    assert np.all(total > 0.0) and np.all(total < 1.0)
+    dv_exact = oracle.matvec(om, res.delta_alpha)
+    assert np.max(np.abs(res.delta_v - dv_exact)) < 1e-9 * max(1.0, np.max(np.abs(dv_exact)))
+    # the exact value of the returned delta matches the solver's tracked value
+    exact = oracle.damped_solve  # noqa: F841 (documenting the oracle used below)
+    w = dv_exact
+    g_val = fv + float(lin @ w) + 0.5 * 2.0 * float(w @ w) + oracle.g_sum(0, 0.5, total)
+    assert g_val == pytest.approx(res.final_subproblem_value, rel=1e-9)
+
+
+def test_gpu_chunk_runner_drop_in(golden):
+    """The reference-facing hook (host buffers through glm_device_solve)."""
+    z = golden("solve")
+    runner = g.gpu_chunk_runner()
+
+    class Dev:
+        pass
+
+    class Cfg:
+        epochs = 0
+        threads_per_device = 1
+
+    for c in range(int(z["n_cases"])):
+        p = f"c{c}_"
+        m = _mat(z, p)
+        tgt = z[p + "target"]
+        kind = KINDS[int(z[p + "kind"])]
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]), 1, 1,
+                               target=tgt if len(tgt) else None)
+        sub = g.LocalSubproblem(spec=spec, lin=z[p + "lin"], quad=float(z[p + "quad"]),
+                                const=float(z[p + "const"]), base=z[p + "base"], data=m,
+                                col_ids=np.arange(m.n_cols))
+        dev = Dev()
+        dev.gen = g.PermutationGenerator(int(z[p + "gen_seed"]))
+        dev.damping = g.DampingState()
+        cfg = Cfg()
+        cfg.epochs = int(z[p + "epochs"])
+        res = runner(sub, dev, cfg)
+        np.testing.assert_allclose(res.epoch_values, z[p + "values"], rtol=1e-11)
+        np.testing.assert_allclose(res.delta_alpha, z[p + "delta"], atol=1e-9)
+        assert dev.gen.state == int(z[p + "gen_state"])
+    runner.close()
+
+
+def test_zero_column_and_empty_edge_cases():
+    # lasso zero column: step -t (test_solver.py:83-87)
+    spec = g.ObjectiveSpec("lasso_primal", 0.5, 3, 1, target=np.zeros(3))
+    assert g.coordinate_update(spec, np.empty(0, np.int32), np.empty(0), 0.0, 0.7,
+                               np.zeros(3), 1.0) == -0.7
+    spec = g.ObjectiveSpec("dual_l2_svm", 1.0, 4, 3)
+    assert g.coordinate_update(spec, np.empty(0, np.int32), np.empty(0), 0.0, 0.2,
+                               np.zeros(3), 1.0) == pytest.approx(0.8)
+    # a matrix whose columns are all empty still solves (values unchanged)
+    m = g.SparseColumnMatrix(3, [0, 0, 0], [], [], validate=False)
+    spec = g.ObjectiveSpec("ridge_primal", 1.0, 3, 2, target=np.ones(3))
+    sub = g.LocalSubproblem(spec=spec, lin=-np.ones(3), quad=1.0, const=1.5, base=np.ones(2),
+                            data=m, col_ids=np.arange(2))
+    res = g.damped_solve(sub, g.PermutationGenerator(1), 2)
+    np.testing.assert_allclose(res.delta_alpha, [-1.0, -1.0])
+    assert math.isfinite(res.final_subproblem_value)
+
+
+def test_solver_error_on_nonfinite_view():
+    m = g.SparseColumnMatrix(2, [0, 1], [0], [1.0])
+    spec = g.ObjectiveSpec("ridge_primal", 1.0, 2, 1, target=np.zeros(2))
+    sub = g.LocalSubproblem(spec=spec, lin=np.array([np.inf, 0.0]), quad=1.0, const=0.0,
+                            base=np.zeros(1), data=m, col_ids=np.arange(1))
+    with pytest.raises(g.SolverError):
+        g.damped_solve(sub, g.PermutationGenerator(1), 1)
+
+
+def test_library_reports_kernels_loaded():
+    lib = _lib.load()
+    assert lib.glm_version() == 1
