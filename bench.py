@@ -262,17 +262,23 @@ def ours_main(args):
     lib = _lib.lib()
     stream = torch.cuda.current_stream()
 
-    for _ in range(args.warmup):
-        eng.outer_round()
-    torch.cuda.synchronize()
-    eng.check_solves()
-    if world > 1:
-        torch.distributed.barrier()
-    wk.solver.timing(True)
-    launches0 = lib.glm_launch_count()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            eng.outer_round()
+        torch.cuda.synchronize()
+        eng.check_solves()
+        # keep the GPU busy while nvidia-smi starts sampling (>= 0.5 s)
+        t_w = time.perf_counter()
+        while time.perf_counter() - t_w < 0.6:
+            for _ in range(20):
+                eng.outer_round()
+            torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        wk.solver.timing(True)
+        launches0 = lib.glm_launch_count()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t_start.record(stream)
         for _ in range(args.steps):
@@ -400,7 +406,7 @@ def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-ttt", action="store_true")

@@ -91,6 +91,11 @@ typedef struct {
     int32_t max_inflight;   /* async: cap on concurrently processed coordinates
                                (0 = auto: min(resident groups, n/32)) */
     int32_t reset_damping;  /* 1: DampingState.reset() before solving (engine.py:251-252) */
+    int32_t accumulate;     /* 1: delta_out += delta, dv_out += B delta (fold in place,
+                               engine.py:264-266, 302-306); 0: overwrite */
+    int32_t flags;          /* async cache policy bits (0 = default): 1 gather the view
+                               through L1; 2 stream the column with L2 evict_first and
+                               keep the view evict_last */
 } glm_solve_args;
 
 /* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */

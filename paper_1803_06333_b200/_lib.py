@@ -34,7 +34,8 @@ class GlmSolveArgs(ctypes.Structure):
     _fields_ = [("kind", _c_i32), ("mode", _c_i32), ("lam", _c_dbl), ("l1_ratio", _c_dbl),
                 ("quad", _c_dbl), ("cnst", _P), ("lin", _P), ("base", _P),
                 ("coord_target", _P), ("epochs", _c_i32), ("max_attempts", _c_i32),
-                ("group_lanes", _c_i32), ("max_inflight", _c_i32), ("reset_damping", _c_i32)]
+                ("group_lanes", _c_i32), ("max_inflight", _c_i32), ("reset_damping", _c_i32),
+                ("accumulate", _c_i32), ("flags", _c_i32)]
 
 
 class GlmSolveResult(ctypes.Structure):

@@ -121,6 +121,7 @@ int glm_solver_destroy(glm_solver *s) {
     cudaFree(s->perm);
     cudaFree(s->perm_mem);
     cudaFree(s->partials);
+    cudaFree(s->gpart);
     cudaFree(s->scratch);
     for (auto &ev : s->events) s->event_pool.push_back(ev);
     for (auto &ev : s->event_pool)
@@ -153,7 +154,8 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     chk(cudaMalloc(&s->perm, sizeof(int32_t) * mc));
     size_t pb = perm_scratch_bytes((int64_t)mc);
     chk(cudaMalloc(&s->perm_mem, pb));
-    chk(cudaMalloc(&s->partials, sizeof(double) * 3 * VALUE_BLOCKS));
+    chk(cudaMalloc(&s->partials, sizeof(double) * 2 * 8 * NUM_SMS));
+    chk(cudaMalloc(&s->gpart, sizeof(double) * 16 * NUM_SMS));
     chk(cudaMalloc(&s->scratch, REDUCE_SCRATCH_BYTES));
     if (e == cudaSuccess) {
         chk(cudaMemset(s->perm_mem, 0, pb));

@@ -33,7 +33,7 @@ struct SolveState {
     int32_t done;
     int32_t dc;               // current delta buffer
     int32_t vw;               // working view buffer
-    int32_t launched;         // attempts enqueued so far (host bookkeeping mirror)
+    int32_t epoch_blocks;     // blocks of the last epoch kernel (g-sum partials)
     uint32_t block_counter;   // last-block-done counter for reductions
     int32_t _pad;
     double epoch_values[MAX_EPOCH_VALUES];
@@ -47,6 +47,44 @@ __device__ __forceinline__ double ld_cg(const double *p) {
 
 __device__ __forceinline__ void red_add(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Cache-policy variants used by the async epoch kernel (flags of glm_solve_args).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_stream_f64(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ld_stream_i32(const int *p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_cg_hint(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_ca_hint(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.ca.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void red_add_hint(double *p, double v, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+                 : "memory");
 }
 
 template <int G>

@@ -35,6 +35,9 @@
 
 namespace glm {
 
+constexpr int EPOCH_PARTIALS = 16 * NUM_SMS;    // >= any epoch grid
+constexpr int VALUE_MAX_BLOCKS = 8 * NUM_SMS;
+
 struct EpochParams {
     SolveState *st;
     int kind;
@@ -49,21 +52,72 @@ struct EpochParams {
     double *delta0, *delta1;
     double *view0, *view1;
     const int32_t *perm;
+    double *gpart;          // per-block partial sum_j g(base_j + delta_j) of the epoch
 };
 
 __device__ __forceinline__ void flag_error(SolveState *st) {
     atomicCAS(&st->status, GLM_OK, GLM_SOLVER_ERROR);
 }
 
+// delta buffers: dc == -1 means "delta is identically zero" (no buffer read);
+// an epoch reads buffer dc and writes buffer (dc == 0 ? 1 : 0).
+__device__ __forceinline__ const double *delta_cur(const EpochParams &p, int dc) {
+    return dc < 0 ? nullptr : (dc ? p.delta1 : p.delta0);
+}
+__device__ __forceinline__ double *delta_next(const EpochParams &p, int dc) {
+    return dc == 0 ? p.delta1 : p.delta0;
+}
+
+// Writes the block's partial g-sum (warp shuffles + smem, fixed order).
+__device__ __forceinline__ void store_block_gsum(double g, double *gpart, SolveState *st) {
+    __shared__ double s_g[32];
+    g = warp_sum(g);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_g[warp] = g;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double x = threadIdx.x < (blockDim.x >> 5) ? s_g[threadIdx.x] : 0.0;
+        x = warp_sum(x);
+        if (threadIdx.x == 0) {
+            gpart[blockIdx.x] = x;
+            if (blockIdx.x == 0) st->epoch_blocks = gridDim.x;
+        }
+    }
+}
+
 // --------------------------------------------------------------- async
-template <int G, bool DENSE>
+// TPA-SCD: a group of G lanes owns coordinate j = perm[k].  The column is
+// loaded once into registers (R elements per lane; longer columns stream the
+// tail), gathered against the shared view through L2, reduced with shuffles,
+// stepped on the group leader, and scattered with red.global.add.f64.
+template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
     if (st->done) return;
+    // CM bit 0: gather the view through L1 (ld.ca); bit 1: stream the column
+    // with L1::no_allocate + L2 evict_first, view traffic evict_last.
+    const uint64_t pol_col = (CM & 2) ? policy_evict_first() : 0;
+    const uint64_t pol_view = (CM & 2) ? policy_evict_last() : 0;
+    auto ld_view = [&](const double *a) -> double {
+        if (CM == 0) return ld_cg(a);
+        if (CM == 1) return __ldca(a);
+        if (CM == 2) return ld_cg_hint(a, pol_view);
+        return ld_ca_hint(a, pol_view);
+    };
+    auto ld_val = [&](const double *a) -> double {
+        return (CM & 2) ? ld_stream_f64(a, pol_col) : __ldg(a);
+    };
+    auto ld_row = [&](const int32_t *a) -> int {
+        return (CM & 2) ? ld_stream_i32(a, pol_col) : __ldg(a);
+    };
+    auto scatter = [&](double *a, double v) {
+        if (CM & 2) red_add_hint(a, v, pol_view);
+        else red_add(a, v);
+    };
     const int dc = st->dc;
     const double damping = st->damping;
-    const double *__restrict__ dcur = dc ? p.delta1 : p.delta0;
-    double *__restrict__ dnext = dc ? p.delta0 : p.delta1;
+    const double *__restrict__ dcur = delta_cur(p, dc);
+    double *__restrict__ dnext = delta_next(p, dc);
     double *view = st->vw ? p.view1 : p.view0;
     constexpr int GPW = 32 / G;
     const int lane = threadIdx.x & 31;
@@ -71,6 +125,7 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int kind = p.kind;
+    double gacc = 0.0;
     for (int64_t kb = warp * GPW; kb < p.m; kb += nwarps * GPW) {
         const int64_t k = kb + sub;
         const bool valid = k < p.m;
@@ -85,34 +140,58 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
                 hi = __ldg(p.indptr + j + 1);
             }
         }
+        // group leader prefetches the coordinate's metadata under the gather
+        double bj = 0.0, dj = 0.0, sj = 0.0, yj = 0.0;
+        if (valid && gl == 0) {
+            bj = __ldg(p.base + j);
+            dj = dcur ? dcur[j] : 0.0;
+            sj = __ldg(p.sq + j);
+            if (p.y) yj = __ldg(p.y + j);
+        }
+        int rr[R];
+        double vv[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t q = lo + gl + i * G;
+            const bool in = q < hi;
+            rr[i] = in ? (DENSE ? (int)(q - lo) : ld_row(p.rows + q)) : 0;
+            vv[i] = in ? ld_val(p.vals + q) : 0.0;
+        }
         double acc = 0.0;
-        for (int64_t q = lo + gl; q < hi; q += G) {
-            const int r = DENSE ? (int)(q - lo) : __ldg(p.rows + q);
-            acc += __ldg(p.vals + q) * ld_cg(view + r);
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (lo + gl + i * G < hi) acc += vv[i] * ld_view(view + rr[i]);
+        for (int64_t q = lo + gl + R * G; q < hi; q += G) {
+            const int r = DENSE ? (int)(q - lo) : ld_row(p.rows + q);
+            acc += ld_val(p.vals + q) * ld_view(view + r);
         }
         const double ga = group_sum<G>(acc);
         double step = 0.0;
         if (valid && gl == 0) {
-            const double dj = dcur[j];
-            const double t = __ldg(p.base + j) + dj;
+            const double t = bj + dj;
             double raw = 0.0;
-            if (!coord_step(kind, p.lam, p.rho, p.y ? __ldg(p.y + j) : 0.0, ga,
-                            p.quad * __ldg(p.sq + j), t, raw)) {
+            if (!coord_step(kind, p.lam, p.rho, yj, ga, p.quad * sj, t, raw)) {
                 flag_error(st);
                 raw = 0.0;
             }
             step = damping * raw;
-            dnext[j] = step != 0.0 ? dj + step : dj;
+            const double dn = step != 0.0 ? dj + step : dj;
+            dnext[j] = dn;
+            gacc += g_one(kind, p.lam, p.rho, yj, bj + dn);
         }
         step = __shfl_sync(0xffffffffu, step, sub * G);
         if (step != 0.0) {
             const double f = p.quad * step;
-            for (int64_t q = lo + gl; q < hi; q += G) {
-                const int r = DENSE ? (int)(q - lo) : __ldg(p.rows + q);
-                red_add(view + r, f * __ldg(p.vals + q));
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (lo + gl + i * G < hi) scatter(view + rr[i], f * vv[i]);
+            for (int64_t q = lo + gl + R * G; q < hi; q += G) {
+                const int r = DENSE ? (int)(q - lo) : ld_row(p.rows + q);
+                scatter(view + r, f * ld_val(p.vals + q));
             }
         }
     }
+    store_block_gsum(gacc, p.gpart, st);
 }
 
 // ----------------------------------------------------------- sequential
@@ -128,8 +207,8 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
     __shared__ double sstep;
     const int dc = st->dc;
     const double damping = st->damping;
-    const double *dcur = dc ? p.delta1 : p.delta0;
-    double *dnext = dc ? p.delta0 : p.delta1;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
     double *gview = st->vw ? p.view1 : p.view0;
     double *V = SMEM ? sview : gview;
     const int t = threadIdx.x;
@@ -138,6 +217,7 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
         __syncthreads();
     }
     const int kind = p.kind;
+    double gacc = 0.0;
     for (int64_t k = 0; k < p.m; ++k) {
         const int j = p.perm[k];
         int64_t lo, hi;
@@ -163,16 +243,18 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
             }
         }
         if (t == 0) {
-            const double dj = dcur[j];
+            const double dj = dcur ? dcur[j] : 0.0;
+            const double yj = p.y ? p.y[j] : 0.0;
             const double tt = p.base[j] + dj;
             double raw = 0.0;
-            if (!coord_step(kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, acc, p.quad * p.sq[j], tt,
-                            raw)) {
+            if (!coord_step(kind, p.lam, p.rho, yj, acc, p.quad * p.sq[j], tt, raw)) {
                 flag_error(st);
                 raw = 0.0;
             }
             const double step = damping * raw;
-            dnext[j] = step != 0.0 ? dj + step : dj;
+            const double dn = step != 0.0 ? dj + step : dj;
+            dnext[j] = dn;
+            gacc += g_one(kind, p.lam, p.rho, yj, p.base[j] + dn);
             sstep = step;
         }
         if (BS > 32) __syncthreads(); else __syncwarp();
@@ -189,6 +271,10 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
     if (SMEM) {
         for (int64_t r = t; r < p.d; r += BS) gview[r] = sview[r];
     }
+    if (t == 0) {
+        p.gpart[0] = gacc;
+        st->epoch_blocks = 1;
+    }
 }
 
 // ------------------------------------------------------- value + decide
@@ -200,41 +286,39 @@ struct ValueParams {
     const double *cnst;
     int64_t m, d;
     const double *lin, *base, *y;
-    double *delta0, *delta1;
     double *view0, *view1;
-    double *partials;
+    double *partials;       // [blocks][2]
+    const double *gpart;    // epoch partial g-sums
 };
 
 // G(delta) = const + lin.w + quad/2 |w|^2 + sum g(base + delta) with
 // quad*w = view - lin, i.e. (lin.u + u.u/2)/quad for u = view - lin
-// (LocalSubproblem.value_given_w, solver.py:132-135).
+// (LocalSubproblem.value_given_w, solver.py:132-135).  The g-sum of an
+// attempt comes from the epoch kernel's block partials; G(0) sums g(base).
 __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
     SolveState *st = p.st;
     if (st->done) return;
-    __shared__ double sm[96];
+    __shared__ double sm[64];
     __shared__ int s_last;
-    const double *dn = p.mode ? (st->dc ? p.delta0 : p.delta1) : nullptr;
     const double *V = st->vw ? p.view1 : p.view0;
-    double acc[3] = {0.0, 0.0, 0.0};
+    double acc[2] = {0.0, 0.0};
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if (p.mode) {
         for (int64_t r = tid; r < p.d; r += nth) {
             const double v = V[r], l = p.lin[r];
-            if (!isfinite(v)) acc[2] += 1.0;
+            if (!isfinite(v)) acc[1] += 1.0;
             const double u = v - l;
             acc[0] += l * u + 0.5 * u * u;
         }
+    } else {
+        for (int64_t j = tid; j < p.m; j += nth)
+            acc[0] += g_one(p.kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, p.base[j]);
     }
-    for (int64_t j = tid; j < p.m; j += nth) {
-        const double tt = p.base[j] + (dn ? dn[j] : 0.0);
-        acc[1] += g_one(p.kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, tt);
-    }
-    block_sum<3>(acc, sm);
+    block_sum<2>(acc, sm);
     if (threadIdx.x == 0) {
-        p.partials[blockIdx.x * 3 + 0] = acc[0];
-        p.partials[blockIdx.x * 3 + 1] = acc[1];
-        p.partials[blockIdx.x * 3 + 2] = acc[2];
+        p.partials[blockIdx.x * 2 + 0] = acc[0];
+        p.partials[blockIdx.x * 2 + 1] = acc[1];
         __threadfence();
         const unsigned ticket = atomicAdd(&st->block_counter, 1u);
         s_last = ticket == gridDim.x - 1;
@@ -242,24 +326,30 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double tot[3] = {0.0, 0.0, 0.0};
+    double tot[2] = {0.0, 0.0};
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-        tot[0] += __ldcg(p.partials + b * 3 + 0);
-        tot[1] += __ldcg(p.partials + b * 3 + 1);
-        tot[2] += __ldcg(p.partials + b * 3 + 2);
+        tot[0] += __ldcg(p.partials + b * 2 + 0);
+        tot[1] += __ldcg(p.partials + b * 2 + 1);
     }
-    block_sum<3>(tot, sm);
+    double gs[1] = {0.0};
+    if (p.mode) {
+        const int eb = st->epoch_blocks;
+        for (int b = threadIdx.x; b < eb; b += blockDim.x) gs[0] += __ldcg(p.gpart + b);
+    }
+    block_sum<2>(tot, sm);
+    block_sum<1>(gs, sm);
     if (threadIdx.x != 0) return;
     st->block_counter = 0;
-    const double G = *p.cnst + (p.mode ? tot[0] / p.quad : 0.0) + tot[1];
     if (!p.mode) {
-        st->value = G;
-        st->initial = G;
+        const double G0 = *p.cnst + tot[0];
+        st->value = G0;
+        st->initial = G0;
         return;
     }
+    const double G = *p.cnst + tot[0] / p.quad + gs[0];
     // damped_solve control flow (solver.py:272-298)
     st->attempts += 1;
-    if (tot[2] > 0.0) {            // solver.py:279-280
+    if (tot[1] > 0.0) {            // solver.py:279-280
         st->status = GLM_SOLVER_ERROR;
         st->done = 1;
         return;
@@ -285,18 +375,17 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
         return;
     }
     st->value = G;
-    st->dc ^= 1;
+    st->dc = st->dc == 0 ? 1 : 0;  // the buffer the epoch wrote
     if (st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
     st->epochs_run += 1;
     if (st->epochs_run >= st->epochs_target) st->done = 1;
 }
 
 // ---------------------------------------------------------- begin / end
-__global__ void begin_kernel(SolveState *st, double *delta0, double *view0, const double *lin,
-                             int64_t m, int64_t d, int epochs, int reset_damping) {
+__global__ void begin_kernel(SolveState *st, double *view0, const double *lin, int64_t d,
+                             int epochs, int reset_damping) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = tid; j < m; j += nth) delta0[j] = 0.0;
     for (int64_t r = tid; r < d; r += nth) view0[r] = lin[r];
     if (tid == 0) {
         st->gen_state = st->gen_next;
@@ -308,9 +397,10 @@ __global__ void begin_kernel(SolveState *st, double *delta0, double *view0, cons
         st->attempts = 0;
         st->status = GLM_OK;
         st->done = 0;
-        st->dc = 0;
+        st->dc = -1;
         st->vw = 0;
         st->block_counter = 0;
+        st->epoch_blocks = 0;
     }
 }
 
@@ -323,19 +413,34 @@ __global__ void snapshot_kernel(const SolveState *st, double *view0, double *vie
     for (int64_t r = tid; r < d; r += nth) dst[r] = src[r];
 }
 
+// Outputs (overwrite or accumulate) + the generator state after the solve.
 __global__ void finalize_kernel(SolveState *st, const double *delta0, const double *delta1,
                                 const double *view0, const double *view1, const double *lin,
                                 double quad, int64_t m, int64_t d, double *delta_out,
-                                double *dv_out) {
-    const double *dl = st->dc ? delta1 : delta0;
+                                double *dv_out, int accumulate) {
+    const int dc = st->dc;
+    const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
     const double *V = st->vw ? view1 : view0;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    if (delta_out)
-        for (int64_t j = tid; j < m; j += nth) delta_out[j] = dl[j];
-    if (dv_out)
-        for (int64_t r = tid; r < d; r += nth) dv_out[r] = (V[r] - lin[r]) / quad;
-    if (tid == 0) st->gen_next = dev_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
+    if (delta_out) {
+        if (accumulate) {
+            if (dl)
+                for (int64_t j = tid; j < m; j += nth) delta_out[j] += dl[j];
+        } else {
+            for (int64_t j = tid; j < m; j += nth) delta_out[j] = dl ? dl[j] : 0.0;
+        }
+    }
+    if (dv_out) {
+        if (accumulate)
+            for (int64_t r = tid; r < d; r += nth) dv_out[r] += (V[r] - lin[r]) / quad;
+        else
+            for (int64_t r = tid; r < d; r += nth) dv_out[r] = (V[r] - lin[r]) / quad;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const uint64_t g = warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
+        if (threadIdx.x == 0) st->gen_next = g;
+    }
 }
 
 __global__ void empty_solve_kernel(SolveState *st) {
@@ -360,12 +465,12 @@ static int grid_stride_blocks(int64_t n) {
     return (int)b;
 }
 
-template <int G, bool DENSE>
+template <int G, int R, bool DENSE, int CM>
 static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s) {
-    static int blocks_per_sm = 0;
+    static int blocks_per_sm = 0;   // identical for every B200
     if (!blocks_per_sm) {
-        GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                                   scd_async<G, DENSE>, 256, 0));
+        GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &blocks_per_sm, scd_async<G, R, DENSE, CM>, 256, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     // Staleness control: at most max_inflight coordinates in flight (default
@@ -374,22 +479,34 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     int64_t groups = max_inflight > 0 ? max_inflight : (p.m + 31) / 32;
     if (groups > p.m) groups = p.m;
     if (groups < 32 / G) groups = 32 / G;
-    int64_t need_blocks = (groups * G + 255) / 256;
+    const int64_t need_blocks = (groups * G + 255) / 256;
     int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
-    int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
+    if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
+    const int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
     count_launch();
-    scd_async<G, DENSE><<<grid, 256, 0, s>>>(p);
+    scd_async<G, R, DENSE, CM><<<grid, 256, 0, s>>>(p);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
 
-template <bool DENSE>
-static int launch_async(const EpochParams &p, int lanes, int max_inflight, cudaStream_t s) {
+template <bool DENSE, int CM>
+static int launch_async_cm(const EpochParams &p, int lanes, int max_inflight, cudaStream_t s) {
     switch (lanes) {
-    case 4: return launch_async_t<4, DENSE>(p, max_inflight, s);
-    case 8: return launch_async_t<8, DENSE>(p, max_inflight, s);
-    case 16: return launch_async_t<16, DENSE>(p, max_inflight, s);
-    default: return launch_async_t<32, DENSE>(p, max_inflight, s);
+    case 4: return launch_async_t<4, 4, DENSE, CM>(p, max_inflight, s);
+    case 8: return launch_async_t<8, 8, DENSE, CM>(p, max_inflight, s);
+    case 16: return launch_async_t<16, 4, DENSE, CM>(p, max_inflight, s);
+    default: return launch_async_t<32, 4, DENSE, CM>(p, max_inflight, s);
+    }
+}
+
+template <bool DENSE>
+static int launch_async(const EpochParams &p, int lanes, int max_inflight, int flags,
+                        cudaStream_t s) {
+    switch (flags & 3) {
+    case 1: return launch_async_cm<DENSE, 1>(p, lanes, max_inflight, s);
+    case 2: return launch_async_cm<DENSE, 2>(p, lanes, max_inflight, s);
+    case 3: return launch_async_cm<DENSE, 3>(p, lanes, max_inflight, s);
+    default: return launch_async_cm<DENSE, 0>(p, lanes, max_inflight, s);
     }
 }
 
@@ -412,10 +529,9 @@ static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
     return GLM_OK;
 }
 
-static int auto_lanes(double avg_nnz) {
-    if (avg_nnz <= 12) return 4;
-    if (avg_nnz <= 24) return 8;
-    if (avg_nnz <= 64) return 16;
+static int auto_lanes(double avg_nnz) {   // lanes x registers cover the column
+    if (avg_nnz <= 16) return 4;
+    if (avg_nnz <= 64) return 8;
     return 32;
 }
 
@@ -489,6 +605,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     ep.view0 = s->view[0];
     ep.view1 = s->view[1];
     ep.perm = s->perm;
+    ep.gpart = s->gpart;
 
     ValueParams vp;
     vp.st = s->st;
@@ -502,22 +619,27 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     vp.lin = a->lin;
     vp.base = a->base;
     vp.y = a->coord_target;
-    vp.delta0 = s->delta[0];
-    vp.delta1 = s->delta[1];
     vp.view0 = s->view[0];
     vp.view1 = s->view[1];
     vp.partials = s->partials;
+    vp.gpart = s->gpart;
 
     const double avg = dense ? (double)d : (m > 0 ? (double)A->nnz / (double)m : 0.0);
     const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg);
     const int seq_bs = avg <= 96.0 ? 32 : 256;
+    auto value_grid = [](int64_t n) {
+        int64_t b = (n + VALUE_THREADS - 1) / VALUE_THREADS;
+        if (b < 1) b = 1;
+        if (b > VALUE_MAX_BLOCKS) b = VALUE_MAX_BLOCKS;
+        return (int)b;
+    };
 
     count_launch();
-    begin_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
-        s->st, s->delta[0], s->view[0], a->lin, m, d, a->epochs, a->reset_damping);
+    begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], a->lin, d,
+                                                            a->epochs, a->reset_damping);
     vp.mode = 0;
     count_launch();
-    value_kernel<<<VALUE_BLOCKS, VALUE_THREADS, 0, stream>>>(vp);
+    value_kernel<<<value_grid(m), VALUE_THREADS, 0, stream>>>(vp);
     GLM_CUDA_TRY(cudaGetLastError());
     vp.mode = 1;
 
@@ -545,13 +667,13 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             if (dense) r = seq_bs == 32 ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
             else r = seq_bs == 32 ? launch_seq_t<32, false>(ep, stream) : launch_seq_t<256, false>(ep, stream);
         } else {
-            r = dense ? launch_async<true>(ep, lanes, a->max_inflight, stream)
-                      : launch_async<false>(ep, lanes, a->max_inflight, stream);
+            r = dense ? launch_async<true>(ep, lanes, a->max_inflight, a->flags, stream)
+                      : launch_async<false>(ep, lanes, a->max_inflight, a->flags, stream);
         }
         if (r) return r;
         if (s->timing) GLM_CUDA_TRY(cudaEventRecord(ev[2], stream));
         count_launch();
-        value_kernel<<<VALUE_BLOCKS, VALUE_THREADS, 0, stream>>>(vp);
+        value_kernel<<<value_grid(d), VALUE_THREADS, 0, stream>>>(vp);
         GLM_CUDA_TRY(cudaGetLastError());
         if (s->timing) {
             GLM_CUDA_TRY(cudaEventRecord(ev[3], stream));
@@ -586,7 +708,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     count_launch();
     finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
-        delta_out, dv_out);
+        delta_out, dv_out, a->accumulate);
     GLM_CUDA_TRY(cudaGetLastError());
     s->last_epochs = a->epochs;
     s->last_m = m;

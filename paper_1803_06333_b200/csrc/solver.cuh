@@ -17,6 +17,7 @@ struct glm_solver {
     int32_t *perm = nullptr;
     void *perm_mem = nullptr;
     double *partials = nullptr;           // value-kernel block partials
+    double *gpart = nullptr;              // epoch-kernel block partial g-sums
     double *scratch = nullptr;            // generic reduction scratch
     int timing = 0;                       // record per-attempt CUDA events
     std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
@@ -26,7 +27,6 @@ struct glm_solver {
 
 namespace glm {
 
-constexpr int VALUE_BLOCKS = 2 * NUM_SMS;   // fixed grid => deterministic sums
 constexpr int VALUE_THREADS = 256;
 constexpr size_t REDUCE_SCRATCH_BYTES = 64 * 1024;
 

@@ -175,7 +175,7 @@ class Engine:
     def __init__(self, matrix, spec, config, reducer=None, cost_model=None, node_index=None,
                  measure_theta_bar=False, measure_theta_outer=False, chunk_runner=None,
                  mode=None, sync_solves=True, retry_budget=2, group_lanes=0, max_inflight=0,
-                 n_total=None):
+                 n_total=None, cache_flags=0):
         if measure_theta_bar or measure_theta_outer:
             raise ValueError("theta measurement is the reference's CPU test-mode oracle "
                              "(solver.py:308-391); it is out of scope on the device path")
@@ -193,6 +193,7 @@ class Engine:
         self.retry_budget = int(retry_budget)
         self.group_lanes = int(group_lanes)
         self.max_inflight = int(max_inflight)
+        self.cache_flags = int(cache_flags)
         local_input = isinstance(matrix, DeviceMatrix) and node_index is not None
         if local_input and n_total is None:
             raise ValueError("a node-local DeviceMatrix needs n_total (global coordinates)")
@@ -318,7 +319,7 @@ class Engine:
                               delta_out=wk.delta, dv_out=wk.dv, coord_target=wk.coord_target,
                               reset_damping=first_inner, max_attempts=max_attempts,
                               group_lanes=self.group_lanes, max_inflight=self.max_inflight,
-                              stream=self.stream)
+                              flags=self.cache_flags, stream=self.stream)
         wk.last = res
 
     def _run_node(self, k):
