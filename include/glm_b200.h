@@ -214,6 +214,11 @@ size_t glm_reduce_scratch_bytes(void);
 /* grad = f'(v) (grad may be NULL); out_fv[0] = f(v) */
 int glm_fgrad(int kind, double lam, const double *target, const double *v, int64_t d,
               double *grad, double *out_fv, double *scratch, void *stream);
+/* Round start (engine.py:271-272) fused with the first inner model (v_bar = 0):
+ * grad = f'(v), lin = grad, out_fv[0] = f(v), cnst_out[0] = f(v) / (K L). */
+int glm_outer_model(int kind, double lam, const double *target, const double *v, int64_t d,
+                    double *grad, double *lin, double *out_fv, double *cnst_out,
+                    double n_nodes, double n_devices, double *scratch, void *stream);
 /* Inner subproblem (engine.py:148-166) with the outer model (engine.py:242-250):
  * lin = grad + qo*vbar; cnst_out = (fv/K + grad.vbar + qo/2 |vbar|^2) / L.
  * vbar may be NULL (= 0). */

@@ -82,6 +82,8 @@ SIGNATURES = {
     "glm_validate": (ctypes.c_int, [_P, _P]),
     "glm_reduce_scratch_bytes": (ctypes.c_size_t, []),
     "glm_fgrad": (ctypes.c_int, [ctypes.c_int, _c_dbl, _P, _P, _c_i64, _P, _P, _P, _P]),
+    "glm_outer_model": (ctypes.c_int, [ctypes.c_int, _c_dbl, _P, _P, _c_i64, _P, _P, _P, _P,
+                                       _c_dbl, _c_dbl, _P, _P]),
     "glm_inner_model": (ctypes.c_int, [_P, _P, _c_i64, _c_dbl, _P, _c_dbl, _c_dbl, _P, _P, _P,
                                        _P]),
     "glm_axpby": (ctypes.c_int, [_c_i64, _c_dbl, _P, _c_dbl, _P, _P]),

@@ -288,6 +288,17 @@ int glm_fgrad(int kind, double lam, const double *target, const double *v, int64
     return GLM_OK;
 }
 
+int glm_outer_model(int kind, double lam, const double *target, const double *v, int64_t d,
+                    double *grad, double *lin, double *out_fv, double *cnst_out,
+                    double n_nodes, double n_devices, double *scratch, void *stream) {
+    count_launch();
+    outer_model_kernel<<<2 * NUM_SMS, 256, 0, S(stream)>>>(kind, lam, target, v, d, grad, lin,
+                                                           out_fv, cnst_out, n_nodes,
+                                                           n_devices, scratch);
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
 int glm_inner_model(const double *grad, const double *vbar, int64_t d, double qo,
                     const double *fv, double n_nodes, double n_devices, double *lin,
                     double *cnst_out, double *scratch, void *stream) {

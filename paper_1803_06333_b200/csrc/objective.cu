@@ -82,6 +82,43 @@ __global__ void __launch_bounds__(RED_THREADS) fgrad_kernel(int kind, double lam
     }
 }
 
+// Outer model at the start of a round fused with the first inner model
+// (engine.py:271-272, 242-250, 148-166 with v_bar = 0): grad = f'(v),
+// lin = grad, fv = f(v), cnst = f(v) / (K L).
+__global__ void __launch_bounds__(RED_THREADS) outer_model_kernel(int kind, double lam,
+                                                                  const double *tgt,
+                                                                  const double *v, int64_t d,
+                                                                  double *grad, double *lin,
+                                                                  double *out_fv, double *cnst,
+                                                                  double K, double L,
+                                                                  double *scratch) {
+    double acc[1] = {0.0};
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const bool dual = kind_is_dual(kind);
+    for (int64_t r = tid; r < d; r += nth) {
+        const double x = v[r];
+        double f, g;
+        if (dual) {
+            f = x * x;
+            g = x / lam;
+        } else {
+            f_terms(kind, lam, tgt[r], x, f, g);
+            if (kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;   // raw square, halved below
+        }
+        acc[0] += f;
+        grad[r] = g;
+        lin[r] = g;
+    }
+    if (reduce_last<1>(acc, scratch)) {
+        double f = acc[0];
+        if (dual) f = f / (2.0 * lam);
+        else if (kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+        *out_fv = f;
+        *cnst = (f / K + 0.0) / L;   // ((fv/K) + grad.0 + 0)/L as engine.py:156-162
+    }
+}
+
 // build_inner_subproblem (engine.py:148-166) with the outer model folded in
 // (engine.py:242-250): lin = grad + qo*vbar; cnst = (fv/K + grad.vbar + qo/2 |vbar|^2)/L
 __global__ void __launch_bounds__(RED_THREADS) inner_model_kernel(

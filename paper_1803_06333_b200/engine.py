@@ -151,11 +151,6 @@ class _Worker:
         self.gen = _GenView(derive_seed(engine.config.seed, seed_index))
         self.damping = _DampView()
         self.solver.set_state(self.gen.state, 1.0, engine.stream)
-        f = dict(dtype=torch.float64, device=engine.device)
-        self.delta = torch.zeros(max(self.m, 1), **f)
-        self.dv = torch.zeros(max(d, 1), **f)
-        self.base = torch.zeros(max(self.m, 1), **f)
-        self.d_slice = torch.zeros(max(self.m, 1), **f)
         self.coord_target = None
         ct = engine.spec.coord_target
         if ct is not None:
@@ -243,6 +238,7 @@ class Engine:
         self.row_target = D.to_device(spec.row_target) if spec.row_target is not None else None
         self.alpha_dev = D.to_device(spec.init_alpha())
         self.v_dev = self._initial_v()
+        self._v0 = self.v_dev.clone()
         self.grad = torch.empty(max(self.d, 1), **f)
         self.lin = torch.empty(max(self.d, 1), **f)
         self.vbar = torch.zeros(max(self.d, 1), **f)
@@ -273,6 +269,16 @@ class Engine:
         out[:self.d] = v[:self.d]
         return out
 
+    def reset(self):
+        """Back to the initial point (engine.py:211-212): alpha0, v0 = A alpha0,
+        fresh permutation streams and damping (no re-upload, no SpMV)."""
+        self.alpha_dev.copy_(_D().to_device(self.spec.init_alpha()))
+        self.v_dev.copy_(self._v0)
+        for (k, l), wk in self.workers.items():
+            wk.gen.state = derive_seed(self.config.seed, k * self.config.devices + l)
+            wk.solver.set_state(wk.gen.state, 1.0, self.stream)
+        self.stamp = 0
+
     @property
     def alpha(self):
         return _D().to_host(self.alpha_dev).copy()
@@ -294,91 +300,95 @@ class Engine:
         return SharedVector(self.v, self.stamp)
 
     # -- one round ---------------------------------------------------------------
-    def _solve_worker(self, wk, lin, cnst, first_inner):
+    def _solve_worker(self, wk, lin, cnst, first_inner, vbar):
+        """One device subtask (engine.py:222-237). The solver folds its result
+        in place: alpha[cols] += delta (the base of the next inner round is then
+        alpha[cols] itself, engine.py:225) and v_bar += Delta v (engine.py:264-266)."""
         cfg = self.config
         D = _D()
-        # base = alpha[cols] + d  (engine.py:225)
-        wk.base[:wk.m].copy_(self.alpha_dev[wk.lo:wk.hi])
-        L.check(L.lib().glm_axpby(wk.m, 1.0, D.ptr(wk.d_slice), 1.0, D.ptr(wk.base),
-                                  D.sptr(self.stream)), "glm_axpby")
         quad = cfg.sigma_bar_eff * cfg.sigma_eff * self.spec.beta
+        a_slice = self.alpha_dev[wk.lo:wk.hi]
         if self.chunk_runner is not None:
             from .solver import LocalSubproblem
             if first_inner:
                 wk.damping.reset()
             sub = LocalSubproblem(spec=self.spec, lin=lin, quad=quad, const=cnst,
-                                  base=wk.base[:wk.m], data=wk.data, col_ids=wk.cols)
+                                  base=a_slice.clone(), data=wk.data, col_ids=wk.cols)
             res = self.chunk_runner(sub, wk, cfg)
-            wk.delta[:wk.m].copy_(D.to_device(res.delta_alpha))
-            wk.dv[:self.d].copy_(D.to_device(res.delta_v))
+            a_slice += D.to_device(res.delta_alpha)
+            vbar[:self.d] += D.to_device(res.delta_v)
             wk.last = res
             return
         max_attempts = 0 if self.sync_solves else cfg.epochs + self.retry_budget
-        res = wk.solver.solve(wk.data, self.spec, lin=lin, cnst=cnst, base=wk.base,
+        res = wk.solver.solve(wk.data, self.spec, lin=lin, cnst=cnst, base=a_slice,
                               quad=quad, epochs=cfg.epochs, mode=self.mode,
-                              delta_out=wk.delta, dv_out=wk.dv, coord_target=wk.coord_target,
+                              delta_out=a_slice, dv_out=vbar, coord_target=wk.coord_target,
                               reset_damping=first_inner, max_attempts=max_attempts,
                               group_lanes=self.group_lanes, max_inflight=self.max_inflight,
-                              flags=self.cache_flags, stream=self.stream)
+                              accumulate=True, flags=self.cache_flags, stream=self.stream)
         wk.last = res
 
-    def _run_node(self, k):
-        """t2 inner rounds for node k (engine.py:239-267); returns v_bar (device)."""
+    def _run_node(self, k, vbar):
+        """t2 inner rounds for node k (engine.py:239-267); accumulates the
+        node's v_bar into `vbar` (zeroed by the caller)."""
         cfg = self.config
         D = _D()
         L_ = cfg.devices
         qo = cfg.sigma_eff * self.spec.beta
-        vbar = self.vbar
-        vbar.zero_()
         wks = [self.workers[(k, l)] for l in range(L_)]
-        for wk in wks:
-            wk.d_slice.zero_()
         for t in range(cfg.t2):
-            # lin = grad + qo*vbar ; cnst = (fv/K + grad.vbar + qo/2|vbar|^2)/L
-            L.check(L.lib().glm_inner_model(D.ptr(self.grad), D.ptr(vbar), self.d, qo,
-                                            D.ptr(self.scal[0:1]), float(cfg.nodes),
-                                            float(L_), D.ptr(self.lin), D.ptr(self.scal[1:2]),
-                                            D.ptr(D.scratch(self.stream)),
-                                            D.sptr(self.stream)), "glm_inner_model")
+            if t > 0 or not self._lin_fresh:
+                # lin = grad + qo*vbar ; cnst = (fv/K + grad.vbar + qo/2|vbar|^2)/L
+                # (t == 0 of a later node: v_bar = 0, rebuild what node k-1 overwrote)
+                L.check(L.lib().glm_inner_model(
+                    D.ptr(self.grad), D.ptr(vbar) if t > 0 else None, self.d, qo,
+                    D.ptr(self.scal[0:1]),
+                    float(cfg.nodes), float(L_), D.ptr(self.lin), D.ptr(self.scal[1:2]),
+                    D.ptr(D.scratch(self.stream)), D.sptr(self.stream)), "glm_inner_model")
             cnst = self.scal[1:2] if self.chunk_runner is None else float(self.scal[1].item())
-            for wk in wks:
-                self._solve_worker(wk, self.lin, cnst, first_inner=(t == 0))
-            for wk in wks:       # canonical device order (engine.py:264-266)
-                L.check(L.lib().glm_axpby(wk.m, 1.0, D.ptr(wk.delta), 1.0, D.ptr(wk.d_slice),
-                                          D.sptr(self.stream)), "glm_axpby")
-                L.check(L.lib().glm_axpby(self.d, 1.0, D.ptr(wk.dv), 1.0, D.ptr(vbar),
-                                          D.sptr(self.stream)), "glm_axpby")
+            # the devices of an inner round read lin/cnst, not v_bar, so folding
+            # each result into v_bar as it lands keeps the reference's device-order
+            # sum (engine.py:264-266) without a second pass
+            self._lin_fresh = False
+            for wk in wks:                       # canonical device order
+                self._solve_worker(wk, self.lin, cnst, first_inner=(t == 0), vbar=vbar)
         return vbar
 
     def outer_round(self):
-        """One outer round (engine.py:269-307)."""
+        """One outer round (engine.py:269-307): grad/f(v) fused with the first
+        inner model, per-node t2 inner rounds, Delta v reduce, v += total."""
         D = _D()
-        L.check(L.lib().glm_fgrad(self.spec.index, self.spec.lam, D.ptr(self.row_target),
-                                  D.ptr(self.v_dev), self.d, D.ptr(self.grad),
-                                  D.ptr(self.scal[0:1]), D.ptr(D.scratch(self.stream)),
-                                  D.sptr(self.stream)), "glm_fgrad")
-        self.total.zero_()
+        cfg = self.config
+        L.check(L.lib().glm_outer_model(
+            self.spec.index, self.spec.lam, D.ptr(self.row_target), D.ptr(self.v_dev), self.d,
+            D.ptr(self.grad), D.ptr(self.lin), D.ptr(self.scal[0:1]), D.ptr(self.scal[1:2]),
+            float(cfg.nodes), float(cfg.devices), D.ptr(D.scratch(self.stream)),
+            D.sptr(self.stream)), "glm_outer_model")
+        self._lin_fresh = True      # lin/cnst hold the t = 0 model (v_bar = 0)
         self.last_results = []
+        single = self.reducer is None and len(self.local_nodes) == 1
         try:
-            for k in self.local_nodes:             # canonical node order
-                vbar = self._run_node(k)
-                if self.reducer is None:
-                    L.check(L.lib().glm_axpby(self.d, 1.0, D.ptr(vbar), 1.0,
+            if single:
+                self.total.zero_()
+                self._run_node(self.local_nodes[0], self.total)
+            elif self.reducer is None:
+                self.total.zero_()
+                for k in self.local_nodes:             # canonical node order (comm.py:41-46)
+                    self.vbar.zero_()
+                    self._run_node(k, self.vbar)
+                    L.check(L.lib().glm_axpby(self.d, 1.0, D.ptr(self.vbar), 1.0,
                                               D.ptr(self.total), D.sptr(self.stream)),
                             "glm_axpby")
-                else:
-                    self.total.copy_(vbar)
-                    self.reducer.allreduce_inplace(self.total)   # engine.py:282
+            else:
+                self.total.zero_()
+                self._run_node(self.local_nodes[0], self.total)
+                self.reducer.allreduce_inplace(self.total)   # engine.py:282
         except BaseException:
             if self.reducer is not None and hasattr(self.reducer, "abort"):
                 self.reducer.abort()
             raise
-        for wk in self.workers.values():          # alpha[cols] += d (engine.py:302-305)
-            L.check(L.lib().glm_axpby(wk.m, 1.0, D.ptr(wk.d_slice), 1.0,
-                                      D.ptr(self.alpha_dev[wk.lo:wk.hi]), D.sptr(self.stream)),
-                    "glm_axpby")
         L.check(L.lib().glm_axpby(self.d, 1.0, D.ptr(self.total), 1.0, D.ptr(self.v_dev),
-                                  D.sptr(self.stream)), "glm_axpby")
+                                  D.sptr(self.stream)), "glm_axpby")   # engine.py:306
         self.stamp += 1
 
     def check_solves(self):
