@@ -93,10 +93,13 @@ typedef struct {
     int32_t reset_damping;  /* 1: DampingState.reset() before solving (engine.py:251-252) */
     int32_t accumulate;     /* 1: delta_out += delta, dv_out += B delta (fold in place,
                                engine.py:264-266, 302-306); 0: overwrite */
-    int32_t flags;          /* async cache policy bits (0 = default): 1 gather the view
-                               through L1; 2 stream the column with L2 evict_first and
-                               keep the view evict_last */
+    int32_t flags;          /* bit 0 / bit 1: async cache policy (1 gather the view through
+                               L1; 2 stream the column L2 evict_first, view evict_last);
+                               GLM_FLAG_REUSE_GSUM: base equals the previous solve's
+                               base + delta (folded in place), reuse its g-sum for G(0) */
 } glm_solve_args;
+
+#define GLM_FLAG_REUSE_GSUM 4
 
 /* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */
 typedef struct {
@@ -171,6 +174,9 @@ int glm_solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *args,
  * kernel, summed over the attempts since the last read; *n_out = attempts. */
 int glm_solver_timing(glm_solver *s, int enable);
 int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out);
+/* Same sums without releasing the events (graph-captured attempts re-record
+ * them on every replay). */
+int glm_solver_timing_peek(glm_solver *s, double *ms_out, int32_t *n_out);
 /* Copy the device-side solve state to the host (synchronises `stream`).
  * epoch_values may be NULL; else capacity >= epochs of the last solve. */
 int glm_solver_result(glm_solver *s, glm_solve_result *res, double *epoch_values,

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libglm_b200.so")
 GLM_OK, GLM_SOLVER_ERROR, GLM_DIVERGENCE, GLM_USAGE, GLM_CUDA_ERROR = range(5)
 CSC, DENSE = 0, 1
 MODE_SEQUENTIAL, MODE_ASYNC = 0, 1
+FLAG_REUSE_GSUM = 4
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32
@@ -52,6 +53,7 @@ SIGNATURES = {
     "glm_launch_count": (ctypes.c_longlong, []),
     "glm_solver_timing": (ctypes.c_int, [_P, ctypes.c_int]),
     "glm_solver_timing_read": (ctypes.c_int, [_P, _P, _P]),
+    "glm_solver_timing_peek": (ctypes.c_int, [_P, _P, _P]),
     "glm_device_count": (ctypes.c_int, [_P]),
     "glm_xorshift_jump": (_c_u64, [_c_u64, _c_u64]),
     "glm_derive_seed": (_c_u64, [_c_u64, _P, ctypes.c_int]),

@@ -65,7 +65,7 @@ int glm_solver_timing(glm_solver *s, int enable) {
     return GLM_OK;
 }
 
-int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out) {
+static int timing_sum(glm_solver *s, double *ms_out, int32_t *n_out, bool consume) {
     if (!s) return glm_set_error(GLM_USAGE, "null solver");
     double acc[3] = {0.0, 0.0, 0.0};
     int n = 0;
@@ -80,11 +80,21 @@ int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out) {
         acc[2] += c;
         ++n;
     }
-    for (auto &ev : s->events) s->event_pool.push_back(ev);
-    s->events.clear();
+    if (consume) {
+        for (auto &ev : s->events) s->event_pool.push_back(ev);
+        s->events.clear();
+    }
     if (ms_out) { ms_out[0] = acc[0]; ms_out[1] = acc[1]; ms_out[2] = acc[2]; }
     if (n_out) *n_out = n;
     return GLM_OK;
+}
+
+int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out) {
+    return timing_sum(s, ms_out, n_out, true);
+}
+
+int glm_solver_timing_peek(glm_solver *s, double *ms_out, int32_t *n_out) {
+    return timing_sum(s, ms_out, n_out, false);
 }
 
 int glm_device_count(int *out) {

@@ -34,6 +34,7 @@ struct SolveState {
     int32_t dc;               // current delta buffer
     int32_t vw;               // working view buffer
     int32_t epoch_blocks;     // blocks of the last epoch kernel (g-sum partials)
+    double gsum_acc;          // sum_j g(base_j + delta_j) of the accepted state
     uint32_t block_counter;   // last-block-done counter for reductions
     int32_t _pad;
     double epoch_values[MAX_EPOCH_VALUES];

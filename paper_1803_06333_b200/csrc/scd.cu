@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
         const double G0 = *p.cnst + tot[0];
         st->value = G0;
         st->initial = G0;
+        st->gsum_acc = tot[0];
         return;
     }
     const double G = *p.cnst + tot[0] / p.quad + gs[0];
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
         return;
     }
     st->value = G;
+    st->gsum_acc = gs[0];
     st->dc = st->dc == 0 ? 1 : 0;  // the buffer the epoch wrote
     if (st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
     st->epochs_run += 1;
@@ -382,12 +384,25 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
 }
 
 // ---------------------------------------------------------- begin / end
-__global__ void begin_kernel(SolveState *st, double *view0, const double *lin, int64_t d,
-                             int epochs, int reset_damping) {
+// Resets the solve state, writes view0 = view1 = lin (the first attempt's
+// snapshot), and — when the caller guarantees base == the previous solve's
+// base + delta (an in-place fold) — takes G(0) = const + the cached g-sum.
+__global__ void begin_kernel(SolveState *st, double *view0, double *view1, const double *lin,
+                             int64_t d, int epochs, int reset_damping, const double *cnst,
+                             int reuse_gsum) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t r = tid; r < d; r += nth) view0[r] = lin[r];
+    for (int64_t r = tid; r < d; r += nth) {
+        const double l = lin[r];
+        view0[r] = l;
+        view1[r] = l;
+    }
     if (tid == 0) {
+        if (reuse_gsum) {
+            const double G0 = *cnst + st->gsum_acc;
+            st->value = G0;
+            st->initial = G0;
+        }
         st->gen_state = st->gen_next;
         if (reset_damping) st->damping = 1.0;
         st->epochs_target = epochs;
@@ -535,6 +550,17 @@ static int auto_lanes(double avg_nnz) {   // lanes x registers cover the column
     return 32;
 }
 
+// Timing events: inside a CUDA-graph capture they become event-record nodes
+// that timestamp every replay (cudaEventRecordExternal).
+static cudaError_t event_record(cudaEvent_t ev, cudaStream_t stream) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(stream, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs == cudaStreamCaptureStatusActive)
+        return cudaEventRecordWithFlags(ev, stream, cudaEventRecordExternal);
+    return cudaEventRecord(ev, stream);
+}
+
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream) {
     count_launch();
     set_state_kernel<<<1, 1, 0, stream>>>(s->st, gen_state ? gen_state : 0x9E3779B97F4A7C15ULL,
@@ -634,13 +660,17 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         return (int)b;
     };
 
+    const int reuse = (a->flags & GLM_FLAG_REUSE_GSUM) ? 1 : 0;
     count_launch();
-    begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], a->lin, d,
-                                                            a->epochs, a->reset_damping);
-    vp.mode = 0;
-    count_launch();
-    value_kernel<<<value_grid(m), VALUE_THREADS, 0, stream>>>(vp);
-    GLM_CUDA_TRY(cudaGetLastError());
+    begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1], a->lin,
+                                                            d, a->epochs, a->reset_damping,
+                                                            a->cnst, reuse);
+    if (!reuse) {
+        vp.mode = 0;
+        count_launch();
+        value_kernel<<<value_grid(m), VALUE_THREADS, 0, stream>>>(vp);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
     vp.mode = 1;
 
     const PermScratch ps = carve_perm_scratch(s->perm_mem, s->max_coords, m);
@@ -655,13 +685,16 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             } else {
                 for (int i = 0; i < 4; ++i) GLM_CUDA_TRY(cudaEventCreate(&ev[i]));
             }
-            GLM_CUDA_TRY(cudaEventRecord(ev[0], stream));
+            GLM_CUDA_TRY(event_record(ev[0], stream));
         }
         int r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, s->perm, ps, stream);
         if (r) return r;
-        if (s->timing) GLM_CUDA_TRY(cudaEventRecord(ev[1], stream));
-        count_launch();
-        snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1], d);
+        if (s->timing) GLM_CUDA_TRY(event_record(ev[1], stream));
+        if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
+            count_launch();
+            snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0],
+                                                                       s->view[1], d);
+        }
         count_launch();
         if (a->mode == GLM_MODE_SEQUENTIAL) {
             if (dense) r = seq_bs == 32 ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
@@ -671,12 +704,12 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
                       : launch_async<false>(ep, lanes, a->max_inflight, a->flags, stream);
         }
         if (r) return r;
-        if (s->timing) GLM_CUDA_TRY(cudaEventRecord(ev[2], stream));
+        if (s->timing) GLM_CUDA_TRY(event_record(ev[2], stream));
         count_launch();
         value_kernel<<<value_grid(d), VALUE_THREADS, 0, stream>>>(vp);
         GLM_CUDA_TRY(cudaGetLastError());
         if (s->timing) {
-            GLM_CUDA_TRY(cudaEventRecord(ev[3], stream));
+            GLM_CUDA_TRY(event_record(ev[3], stream));
             s->events.push_back(ev);
         }
         ++launched;

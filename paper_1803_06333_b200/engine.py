@@ -151,6 +151,7 @@ class _Worker:
         self.gen = _GenView(derive_seed(engine.config.seed, seed_index))
         self.damping = _DampView()
         self.solver.set_state(self.gen.state, 1.0, engine.stream)
+        self.gsum_ok = False        # solver's cached g-sum matches alpha[cols]
         self.coord_target = None
         ct = engine.spec.coord_target
         if ct is not None:
@@ -277,7 +278,31 @@ class Engine:
         for (k, l), wk in self.workers.items():
             wk.gen.state = derive_seed(self.config.seed, k * self.config.devices + l)
             wk.solver.set_state(wk.gen.state, 1.0, self.stream)
+            wk.gsum_ok = False
         self.stamp = 0
+
+    def capture(self, rounds):
+        """Record `rounds` outer rounds from the current state as one CUDA graph
+        (requires sync_solves=False: no host round-trip inside a round; the
+        NCCL all-reduce is captured too). Replay after reset():
+        ``g = eng.capture(20); eng.reset(); g.replay()``. The graph's first
+        round computes G(0) from scratch, so call this right after reset()."""
+        if self.sync_solves or self.chunk_runner is not None:
+            raise ValueError("graph capture needs sync_solves=False and the device solver")
+        D = _D()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        D.scratch(side)                        # allocate outside the capture
+        graph = torch.cuda.CUDAGraph()
+        prev = self.stream
+        try:
+            with torch.cuda.graph(graph, stream=side):
+                self.stream = torch.cuda.current_stream()
+                for _ in range(rounds):
+                    self.outer_round()
+        finally:
+            self.stream = prev
+        return graph
 
     @property
     def alpha(self):
@@ -286,6 +311,8 @@ class Engine:
     @alpha.setter
     def alpha(self, value):
         self.alpha_dev = _D().to_device(value).clone()
+        for wk in self.workers.values():
+            wk.gsum_ok = False
 
     @property
     def v(self):
@@ -320,12 +347,15 @@ class Engine:
             wk.last = res
             return
         max_attempts = 0 if self.sync_solves else cfg.epochs + self.retry_budget
+        flags = self.cache_flags | (L.FLAG_REUSE_GSUM if wk.gsum_ok else 0)
         res = wk.solver.solve(wk.data, self.spec, lin=lin, cnst=cnst, base=a_slice,
                               quad=quad, epochs=cfg.epochs, mode=self.mode,
                               delta_out=a_slice, dv_out=vbar, coord_target=wk.coord_target,
                               reset_damping=first_inner, max_attempts=max_attempts,
                               group_lanes=self.group_lanes, max_inflight=self.max_inflight,
-                              accumulate=True, flags=self.cache_flags, stream=self.stream)
+                              accumulate=True, flags=flags, stream=self.stream)
+        # alpha[cols] now holds base + delta, whose g-sum the solver cached
+        wk.gsum_ok = True
         wk.last = res
 
     def _run_node(self, k, vbar):

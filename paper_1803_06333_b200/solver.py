@@ -261,13 +261,14 @@ class DeviceSolver:
     def timing(self, enable=True):
         L.check(L.lib().glm_solver_timing(self.handle, 1 if enable else 0), "glm_solver_timing")
 
-    def timing_read(self):
-        """(perm_ms, epoch_ms, value_ms) summed over attempts, attempts."""
+    def timing_read(self, consume=True):
+        """(perm_ms, epoch_ms, value_ms) summed over attempts, attempts.
+        consume=False keeps graph-captured events for the next replay."""
         ms = np.zeros(3)
         n = np.zeros(1, dtype=np.int32)
-        L.check(L.lib().glm_solver_timing_read(self.handle, ms.ctypes.data_as(ctypes.c_void_p),
-                                               n.ctypes.data_as(ctypes.c_void_p)),
-                "glm_solver_timing_read")
+        fn = L.lib().glm_solver_timing_read if consume else L.lib().glm_solver_timing_peek
+        L.check(fn(self.handle, ms.ctypes.data_as(ctypes.c_void_p),
+                   n.ctypes.data_as(ctypes.c_void_p)), "glm_solver_timing_read")
         return ms, int(n[0])
 
     def result(self, stream=None):
