@@ -232,9 +232,18 @@ def config_block(world):
 
 
 # ------------------------------------------------------------ GPU arm
+T_START = time.perf_counter()
+
+
+def phase(msg, rank=0):
+    print(f"[bench r{rank} +{time.perf_counter() - T_START:7.1f}s] {msg}", file=sys.stderr,
+          flush=True)
+
+
 def ours_main(args):
     import torch
     world, rank, local = dist_setup()
+    phase(f"dist up (world {world})", rank)
     import paper_1803_06333_b200 as g
     from paper_1803_06333_b200 import _lib
     from paper_1803_06333_b200.comm import NcclReducer
@@ -249,6 +258,7 @@ def ours_main(args):
     indptr, rows, vals, y = gen_columns(lo_b, hi_b)
     m_loc = len(y)
     nnz_loc = int(indptr[-1])
+    phase("data generated", rank)
     dm = DeviceMatrix.from_csc(D_FEAT, indptr, rows, vals)
     spec = g.ObjectiveSpec("dual_l2_logistic", LAM, N_EX, D_FEAT)
     reducer = NcclReducer() if world > 1 else None
@@ -261,6 +271,7 @@ def ours_main(args):
                         cache_flags=args.cache_flags)
 
     eng = make_engine()
+    phase("engine ready", rank)
     wk = next(iter(eng.workers.values()))
     lib = _lib.lib()
     stream = torch.cuda.current_stream()
@@ -313,6 +324,7 @@ def ours_main(args):
         torch.cuda.synchronize()
         return t0.elapsed_time(t1)
 
+    phase("warm-up + capture done", rank)
     kern_ms = np.zeros(3)
     attempts = 0
     with ClockSampler(local) as clk:
@@ -361,9 +373,11 @@ def ours_main(args):
                                       "value_damping": kern_ms[2] / max(attempts, 1),
                                       "step": ms_step}}
 
+    phase("timed region done", rank)
     # -------- e2e through the reference-facing C-ABI with host buffers
     e2e = e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world)
 
+    phase("e2e done", rank)
     # -------- time to 1e-3 suboptimality (certified by the duality gap)
     ttt = None
     if not args.no_ttt:

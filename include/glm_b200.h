@@ -100,6 +100,10 @@ typedef struct {
 } glm_solve_args;
 
 #define GLM_FLAG_REUSE_GSUM 4
+/* After the solve, generate the next solve's first permutation on a side
+ * stream (from the advanced generator state) so it overlaps the caller's
+ * fold / all-reduce; the next glm_solve of the same solver consumes it. */
+#define GLM_FLAG_PREFETCH_PERM 8
 
 /* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */
 typedef struct {
@@ -177,6 +181,9 @@ int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out);
 /* Same sums without releasing the events (graph-captured attempts re-record
  * them on every replay). */
 int glm_solver_timing_peek(glm_solver *s, double *ms_out, int32_t *n_out);
+/* Make `stream` wait for a pending permutation prefetch (before ending a
+ * graph capture or reusing the solver from another stream). */
+int glm_solver_join(glm_solver *s, void *stream);
 /* Copy the device-side solve state to the host (synchronises `stream`).
  * epoch_values may be NULL; else capacity >= epochs of the last solve. */
 int glm_solver_result(glm_solver *s, glm_solve_result *res, double *epoch_values,

@@ -18,6 +18,7 @@ GLM_OK, GLM_SOLVER_ERROR, GLM_DIVERGENCE, GLM_USAGE, GLM_CUDA_ERROR = range(5)
 CSC, DENSE = 0, 1
 MODE_SEQUENTIAL, MODE_ASYNC = 0, 1
 FLAG_REUSE_GSUM = 4
+FLAG_PREFETCH_PERM = 8
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32
@@ -68,6 +69,7 @@ SIGNATURES = {
     "glm_solver_set_state": (ctypes.c_int, [_P, _c_u64, _c_dbl, _P]),
     "glm_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "glm_solver_result": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, _P]),
+    "glm_solver_join": (ctypes.c_int, [_P, _P]),
     "glm_perm_keys": (ctypes.c_int, [_c_u64, _c_i64, _P, _P]),
     "glm_chunk_keys": (ctypes.c_int, [_c_u64, _c_i64, _P, _P]),
     "glm_argsort_temp_bytes": (ctypes.c_size_t, [_c_i64]),

@@ -122,6 +122,7 @@ int glm_solver_destroy(glm_solver *s) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
+    cudaDeviceSynchronize();
     cudaFree(s->st);
     cudaFreeHost(s->st_host);
     cudaFree(s->delta[0]);
@@ -133,6 +134,12 @@ int glm_solver_destroy(glm_solver *s) {
     cudaFree(s->partials);
     cudaFree(s->gpart);
     cudaFree(s->scratch);
+    if (s->side) {
+        cudaStreamSynchronize(s->side);
+        cudaStreamDestroy(s->side);
+        cudaEventDestroy(s->ev_fork);
+        cudaEventDestroy(s->ev_join);
+    }
     for (auto &ev : s->events) s->event_pool.push_back(ev);
     for (auto &ev : s->event_pool)
         for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
@@ -203,6 +210,11 @@ int glm_solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *args, do
         return res->status;
     }
     return GLM_OK;
+}
+
+int glm_solver_join(glm_solver *s, void *stream) {
+    if (!s) return glm_set_error(GLM_USAGE, "null solver");
+    return join_prefetch(s, S(stream));
 }
 
 int glm_solver_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int capacity,

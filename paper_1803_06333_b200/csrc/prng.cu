@@ -145,12 +145,13 @@ __device__ __forceinline__ uint64_t dev_derive1(uint64_t base, uint64_t ix) {
 // Key sources: block_base() returns the state before the block's first key
 // (called by the 32 lanes of warp 0).
 struct StreamKeys {       // PermutationGenerator stream at attempt offset
-    const SolveState *st; // non-null: base state = st->gen_state, skip once done
+    const SolveState *st; // non-null: skip once st->done
+    const uint64_t *state_ptr;   // device-held start state (else `state`)
     uint64_t state;
     uint64_t offset;
     __device__ __forceinline__ bool skip() const { return st && st->done; }
     __device__ __forceinline__ uint64_t block_base() const {
-        const uint64_t s0 = st ? st->gen_state : state;
+        const uint64_t s0 = state_ptr ? *state_ptr : state;
         return warp_jump(s0, offset + (uint64_t)blockIdx.x * KEYS_PER_BLOCK);
     }
 };
@@ -405,8 +406,14 @@ static int perm_from_source(const Src &src, const SolveState *st, int64_t n, int
 
 int stream_perm(const SolveState *st, uint64_t state, uint64_t offset, int64_t n,
                 int32_t *perm, const PermScratch &sc, cudaStream_t stream) {
-    StreamKeys src{st, state, offset};
+    StreamKeys src{st, st ? &st->gen_state : nullptr, state, offset};
     return perm_from_source(src, st, n, perm, sc, stream, nullptr);
+}
+
+int stream_perm_from(const uint64_t *state_dev, int64_t n, int32_t *perm, const PermScratch &sc,
+                     cudaStream_t stream) {
+    StreamKeys src{nullptr, state_dev, 0, 0};
+    return perm_from_source(src, nullptr, n, perm, sc, stream, nullptr);
 }
 
 int chunk_perm(uint64_t seed, int64_t n, int32_t *perm, const PermScratch &sc,
@@ -424,7 +431,7 @@ int array_perm(const uint32_t *keys, int64_t n, int32_t *perm, const PermScratch
 int stream_keys(uint64_t state, uint64_t offset, int64_t n, uint32_t *keys,
                 cudaStream_t stream) {
     if (n <= 0) return GLM_OK;
-    StreamKeys src{nullptr, state, offset};
+    StreamKeys src{nullptr, nullptr, state, offset};
     count_launch();
     keys_kernel<<<key_blocks(n), PERM_THREADS, 0, stream>>>(src, n, keys);
     GLM_CUDA_TRY(cudaGetLastError());

@@ -26,6 +26,9 @@ PermScratch carve_perm_scratch(void *base, int64_t capacity, int64_t n);
 // st->gen_state (st != nullptr; kernels skip once st->done) or `state`.
 int stream_perm(const SolveState *st, uint64_t state, uint64_t offset, int64_t n,
                 int32_t *perm, const PermScratch &sc, cudaStream_t stream);
+// Permutation of the stream starting at the device-held state *state_dev.
+int stream_perm_from(const uint64_t *state_dev, int64_t n, int32_t *perm,
+                     const PermScratch &sc, cudaStream_t stream);
 int chunk_perm(uint64_t seed, int64_t n, int32_t *perm, const PermScratch &sc,
                cudaStream_t stream);
 int array_perm(const uint32_t *keys, int64_t n, int32_t *perm, const PermScratch &sc,

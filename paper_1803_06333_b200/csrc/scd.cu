@@ -53,6 +53,7 @@ struct EpochParams {
     double *view0, *view1;
     const int32_t *perm;
     double *gpart;          // per-block partial sum_j g(base_j + delta_j) of the epoch
+    int64_t nnz;
 };
 
 __device__ __forceinline__ void flag_error(SolveState *st) {
@@ -491,7 +492,12 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     // Staleness control: at most max_inflight coordinates in flight (default
     // n/32, i.e. ~3% of the partition) — the GPU analogue of the reference's
     // thread count (solver.py:213-239).  Large partitions fill the GPU.
-    int64_t groups = max_inflight > 0 ? max_inflight : (p.m + 31) / 32;
+    int64_t groups = max_inflight;
+    if (groups <= 0) {   // feature-conflict budget: ~16 * d / nnz coordinates in flight
+        const double avg = DENSE ? (double)p.d : (double)p.nnz / (double)(p.m > 0 ? p.m : 1);
+        groups = (int64_t)(16.0 * (double)p.d / (avg > 1.0 ? avg : 1.0));
+        if (groups < 32) groups = 32;
+    }
     if (groups > p.m) groups = p.m;
     if (groups < 32 / G) groups = 32 / G;
     const int64_t need_blocks = (groups * G + 255) / 256;
@@ -561,7 +567,20 @@ static cudaError_t event_record(cudaEvent_t ev, cudaStream_t stream) {
     return cudaEventRecord(ev, stream);
 }
 
+// The prefetch branch (side stream) must rejoin `stream` before the solver's
+// scratch is reused or a graph capture ends.
+// A join retires the prefetch: its event may have been recorded inside a graph
+// capture and must not be waited on again outside it.
+int join_prefetch(glm_solver *s, cudaStream_t stream) {
+    if (s->prefetched) GLM_CUDA_TRY(cudaStreamWaitEvent(stream, s->ev_join, 0));
+    s->prefetched = false;
+    return GLM_OK;
+}
+
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream) {
+    int rc = join_prefetch(s, stream);
+    if (rc) return rc;
+    s->prefetched = false;               // the stream state changes
     count_launch();
     set_state_kernel<<<1, 1, 0, stream>>>(s->st, gen_state ? gen_state : 0x9E3779B97F4A7C15ULL,
                                           damping);
@@ -632,6 +651,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     ep.view1 = s->view[1];
     ep.perm = s->perm;
     ep.gpart = s->gpart;
+    ep.nnz = A->nnz;
 
     ValueParams vp;
     vp.st = s->st;
@@ -674,6 +694,14 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     vp.mode = 1;
 
     const PermScratch ps = carve_perm_scratch(s->perm_mem, s->max_coords, m);
+    // a permutation prefetched by the previous solve (GLM_FLAG_PREFETCH_PERM)
+    // is this solve's attempt 0 when it was generated for the same m
+    bool have_perm0 = false;
+    if (s->prefetched) {
+        GLM_CUDA_TRY(cudaStreamWaitEvent(stream, s->ev_join, 0));
+        have_perm0 = s->prefetch_m == m;
+        s->prefetched = false;
+    }
     int launched = 0;
     auto attempt = [&]() -> int {
         // optional CUDA-event bracket: [perm | snapshot+epoch | value]
@@ -687,7 +715,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             }
             GLM_CUDA_TRY(event_record(ev[0], stream));
         }
-        int r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, s->perm, ps, stream);
+        int r = GLM_OK;
+        if (!(launched == 0 && have_perm0))
+            r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, s->perm, ps, stream);
         if (r) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[1], stream));
         if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
@@ -745,6 +775,22 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     GLM_CUDA_TRY(cudaGetLastError());
     s->last_epochs = a->epochs;
     s->last_m = m;
+    if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0) {
+        // generate the next solve's attempt-0 permutation from gen_next while the
+        // caller runs its fold / all-reduce / round-start kernels
+        if (!s->side) {
+            GLM_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        }
+        GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+        GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+        rc = stream_perm_from(&s->st->gen_next, m, s->perm, ps, s->side);
+        if (rc) return rc;
+        GLM_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
+        s->prefetched = true;
+        s->prefetch_m = m;
+    }
     if (res) return read_result(s, res, nullptr, 0, stream);
     return GLM_OK;
 }

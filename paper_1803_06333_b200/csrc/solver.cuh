@@ -20,6 +20,10 @@ struct glm_solver {
     double *gpart = nullptr;              // epoch-kernel block partial g-sums
     double *scratch = nullptr;            // generic reduction scratch
     int timing = 0;                       // record per-attempt CUDA events
+    cudaStream_t side = nullptr;          // permutation prefetch stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool prefetched = false;              // perm holds the next solve's attempt 0
+    int64_t prefetch_m = 0;
     std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
     int last_epochs = 0;
     int64_t last_m = 0;
@@ -35,5 +39,6 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
 int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int cap,
                 cudaStream_t stream);
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
+int join_prefetch(glm_solver *s, cudaStream_t stream);
 
 }  // namespace glm

@@ -300,6 +300,8 @@ class Engine:
                 self.stream = torch.cuda.current_stream()
                 for _ in range(rounds):
                     self.outer_round()
+                for wk in self.workers.values():   # rejoin the prefetch branches
+                    wk.solver.join(self.stream)
         finally:
             self.stream = prev
         return graph
@@ -347,7 +349,8 @@ class Engine:
             wk.last = res
             return
         max_attempts = 0 if self.sync_solves else cfg.epochs + self.retry_budget
-        flags = self.cache_flags | (L.FLAG_REUSE_GSUM if wk.gsum_ok else 0)
+        flags = self.cache_flags | L.FLAG_PREFETCH_PERM | (L.FLAG_REUSE_GSUM if wk.gsum_ok
+                                                              else 0)
         res = wk.solver.solve(wk.data, self.spec, lin=lin, cnst=cnst, base=a_slice,
                               quad=quad, epochs=cfg.epochs, mode=self.mode,
                               delta_out=a_slice, dv_out=vbar, coord_target=wk.coord_target,

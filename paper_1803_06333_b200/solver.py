@@ -258,6 +258,10 @@ class DeviceSolver:
         L.check(st, "glm_solve")
         return res if max_attempts == 0 else None
 
+    def join(self, stream=None):
+        """Make `stream` wait for this solver's pending permutation prefetch."""
+        L.check(L.lib().glm_solver_join(self.handle, _D().sptr(stream)), "glm_solver_join")
+
     def timing(self, enable=True):
         L.check(L.lib().glm_solver_timing(self.handle, 1 if enable else 0), "glm_solver_timing")
 
