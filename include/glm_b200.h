@@ -262,6 +262,77 @@ int glm_coordinate_steps(int kind, double lam, double l1_ratio, const double *y,
                          const double *ga, const double *c, const double *t, int64_t n,
                          double *step, void *stream);
 
+/* ------------------------------------ (3) out-of-core streaming pipeline
+ * Replaces chunked_device_runner / pipelined_epoch / _train_chunk
+ * (/root/reference/pkg/src/hierglm/pipeline.py:158-340): the engine's
+ * chunk_runner hook (engine.py:228-229) for a device partition cut into
+ * chunks.  Chunks within `device_budget` bytes stay resident in HBM (<= 0:
+ * all resident); the rest stream every epoch through two device slots,
+ * double-buffered against the solve (loader thread -> pinned staging ->
+ * cudaMemcpyAsync on a copy stream).  Per chunk: keys
+ * generate_keys(derive_seed(seed, epoch_index + e, chunk)) (pipeline.py:
+ * 226-227), stable argsort, one damped pass with chunk-granular
+ * restore / plateau / halve / divergence (pipeline.py:180-193). */
+typedef struct glm_stream glm_stream;
+
+#define GLM_STREAM_DELTA_IN 16   /* delta_io holds the starting delta (else zero) */
+#define GLM_STREAM_VIEW_IN 32    /* view_io holds the starting view (else lin) */
+#define GLM_STREAM_TIMING 64     /* record the per-chunk schedule (glm_stream_schedule) */
+#define GLM_STREAM_SCHED_COLS 6  /* epoch, chunk, load_ms, h2d_ms, train_ms, t_ms */
+
+typedef struct {
+    int32_t kind;
+    int32_t mode;               /* glm_mode: per-chunk run_pass n_threads==1 / > 1 */
+    double lam;
+    double l1_ratio;
+    double quad;
+    double cnst;                /* LocalSubproblem.const of the whole device partition */
+    const double *lin;          /* f64[n_rows]  (host or device memory) */
+    const double *base;         /* f64[n_cols]  (host or device memory) */
+    const double *coord_target; /* f64[n_cols] or NULL */
+    uint64_t seed;              /* chunked_device_runner(store, seed, ...) */
+    uint64_t epoch_index;       /* the runner's global epoch counter at this call */
+    int32_t epochs;
+    int32_t attempts_per_chunk; /* attempts enqueued ahead per chunk (0 = 2) */
+    int32_t group_lanes;
+    int32_t max_inflight;
+    int32_t flags;              /* bits 0-1 cache policy (glm_solve_args.flags), GLM_STREAM_* */
+    int32_t _pad;
+} glm_stream_args;
+
+/* Host CSC arrays (pinned arrays are DMA'd directly; pin_host=1 registers
+ * pageable arrays, else they are staged through pinned buffers); chunk c =
+ * columns [col_offsets[c], col_offsets[c+1]).  The arrays must outlive the
+ * stream. */
+int glm_stream_create_host(int device, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
+                           const int32_t *rows, const double *vals, int n_chunks,
+                           const int64_t *col_offsets, int64_t device_budget, int pin_host,
+                           glm_stream **out);
+/* A GLMCHUNK v1 file (data.py:307-431) read with pread by the loader thread:
+ * chunk_offsets = ChunkDescriptor.offset (the <IQ chunk head) as scanned by
+ * open_chunks (data.py:362-398). */
+int glm_stream_create_file(int device, const char *path, int64_t n_rows, int n_chunks,
+                           const int64_t *chunk_offsets, const int64_t *chunk_cols,
+                           const int64_t *chunk_nnz, int64_t device_budget, glm_stream **out);
+int glm_stream_destroy(glm_stream *s);
+/* out[7] = n_chunks, resident chunks, resident bytes, streaming-slot bytes,
+ * direct DMA (0/1), n_cols, n_rows */
+int glm_stream_info(const glm_stream *s, int64_t *out);
+/* `epochs` passes over every chunk (chunked_device_runner's runner body).
+ * delta_io f64[n_cols] (in with GLM_STREAM_DELTA_IN; out: the partition's
+ * Delta alpha), view_io f64[n_rows] or NULL (the running view, in with
+ * GLM_STREAM_VIEW_IN), dv_out = B delta = (view - lin)/quad or NULL,
+ * values_out[epochs] = device value after each epoch, info_out[5] =
+ * epochs_run, retries, plateaued chunks, attempts, status; scal_out[4] =
+ * initial value, final value, wall ms, ms the solve waited for loads.
+ * Pointers may be host or device memory. */
+int glm_stream_solve(glm_stream *s, const glm_stream_args *args, double *damping_io,
+                     double *delta_io, double *view_io, double *dv_out, double *values_out,
+                     int32_t *info_out, double *scal_out);
+/* Per-chunk schedule of the last solve with GLM_STREAM_TIMING (PipelineSchedule,
+ * pipeline.py:81-138): GLM_STREAM_SCHED_COLS doubles per chunk. */
+int glm_stream_schedule(const glm_stream *s, double *out, int capacity_rows, int *n_rows_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@ CSC, DENSE = 0, 1
 MODE_SEQUENTIAL, MODE_ASYNC = 0, 1
 FLAG_REUSE_GSUM = 4
 FLAG_PREFETCH_PERM = 8
+STREAM_DELTA_IN, STREAM_VIEW_IN, STREAM_TIMING = 16, 32, 64
+STREAM_SCHED_COLS = 6
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32
@@ -45,6 +47,14 @@ class GlmSolveResult(ctypes.Structure):
                 ("plateaued", _c_i32), ("attempts", _c_i32), ("done", _c_i32),
                 ("damping", _c_dbl), ("initial_value", _c_dbl), ("final_value", _c_dbl),
                 ("gen_state", _c_u64)]
+
+
+class GlmStreamArgs(ctypes.Structure):
+    _fields_ = [("kind", _c_i32), ("mode", _c_i32), ("lam", _c_dbl), ("l1_ratio", _c_dbl),
+                ("quad", _c_dbl), ("cnst", _c_dbl), ("lin", _P), ("base", _P),
+                ("coord_target", _P), ("seed", _c_u64), ("epoch_index", _c_u64),
+                ("epochs", _c_i32), ("attempts_per_chunk", _c_i32), ("group_lanes", _c_i32),
+                ("max_inflight", _c_i32), ("flags", _c_i32), ("_pad", _c_i32)]
 
 
 # name -> (restype, argtypes); every symbol of include/glm_b200.h
@@ -97,6 +107,14 @@ SIGNATURES = {
     "glm_predict": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, _P, _P, _P, _P, _P]),
     "glm_coordinate_steps": (ctypes.c_int, [ctypes.c_int, _c_dbl, _c_dbl, _P, _P, _P, _P, _c_i64,
                                             _P, _P]),
+    "glm_stream_create_host": (ctypes.c_int, [ctypes.c_int, _c_i64, _c_i64, _P, _P, _P,
+                                              ctypes.c_int, _P, _c_i64, ctypes.c_int, _P]),
+    "glm_stream_create_file": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _c_i64, ctypes.c_int,
+                                              _P, _P, _P, _c_i64, _P]),
+    "glm_stream_destroy": (ctypes.c_int, [_P]),
+    "glm_stream_info": (ctypes.c_int, [_P, _P]),
+    "glm_stream_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "glm_stream_schedule": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
 }
 
 _LIB = None

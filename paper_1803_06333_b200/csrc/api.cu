@@ -171,7 +171,7 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     chk(cudaMalloc(&s->perm, sizeof(int32_t) * mc));
     size_t pb = perm_scratch_bytes((int64_t)mc);
     chk(cudaMalloc(&s->perm_mem, pb));
-    chk(cudaMalloc(&s->partials, sizeof(double) * 2 * 8 * NUM_SMS));
+    chk(cudaMalloc(&s->partials, sizeof(double) * 3 * 8 * NUM_SMS));
     chk(cudaMalloc(&s->gpart, sizeof(double) * 16 * NUM_SMS));
     chk(cudaMalloc(&s->scratch, REDUCE_SCRATCH_BYTES));
     if (e == cudaSuccess) {

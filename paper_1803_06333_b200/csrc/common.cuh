@@ -37,6 +37,11 @@ struct SolveState {
     double gsum_acc;          // sum_j g(base_j + delta_j) of the accepted state
     uint32_t block_counter;   // last-block-done counter for reductions
     int32_t _pad;
+    // chunked (out-of-core) mode, pipeline.py:158-197: the chunk being solved
+    // (a sequence number over epochs x chunks; -1 before the first) and the
+    // g-sum of its coordinates in the accepted state.
+    int64_t seq;
+    double gsum_old;
     double epoch_values[MAX_EPOCH_VALUES];
 };
 

@@ -5,3 +5,4 @@
 #include "objective.cu"
 #include "data.cu"
 #include "api.cu"
+#include "stream.cu"

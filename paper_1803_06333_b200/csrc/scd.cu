@@ -54,7 +54,14 @@ struct EpochParams {
     const int32_t *perm;
     double *gpart;          // per-block partial sum_j g(base_j + delta_j) of the epoch
     int64_t nnz;
+    int64_t seq;            // chunked mode: run only while chunk `seq` is open (-1: always)
 };
+
+// A kernel of chunk `seq` runs only while that chunk is open and unfinished;
+// seq < 0 (in-memory solves) only tests `done`.
+__device__ __forceinline__ bool skip_attempt(const SolveState *st, int64_t seq) {
+    return st->done || (seq >= 0 && st->seq != seq);
+}
 
 __device__ __forceinline__ void flag_error(SolveState *st) {
     atomicCAS(&st->status, GLM_OK, GLM_SOLVER_ERROR);
@@ -94,7 +101,7 @@ __device__ __forceinline__ void store_block_gsum(double g, double *gpart, SolveS
 template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
-    if (st->done) return;
+    if (skip_attempt(st, p.seq)) return;
     // CM bit 0: gather the view through L1 (ld.ca); bit 1: stream the column
     // with L1::no_allocate + L2 evict_first, view traffic evict_last.
     const uint64_t pol_col = (CM & 2) ? policy_evict_first() : 0;
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
 template <int BS, bool SMEM, bool DENSE>
 __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
     SolveState *st = p.st;
-    if (st->done) return;
+    if (skip_attempt(st, p.seq)) return;
     extern __shared__ double sview[];
     __shared__ double sred[32];
     __shared__ double sstep;
@@ -281,14 +288,18 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
 // ------------------------------------------------------- value + decide
 struct ValueParams {
     SolveState *st;
-    int mode;   // 0: initial G(0); 1: after an attempt
+    int mode;   // 0: initial G; 1: after an attempt; 2: chunk g-sum of the accepted state
     int kind;
     double lam, rho, quad;
     const double *cnst;
     int64_t m, d;
     const double *lin, *base, *y;
+    const double *dfull;    // modes 0/2: delta added to base (NULL = 0)
+    int view_terms;         // mode 0: include (lin.u + u.u/2)/quad, u = view - lin
+    int chunked;            // mode 1: G uses gsum_acc - gsum_old + the chunk's new g-sum
+    int64_t seq;
     double *view0, *view1;
-    double *partials;       // [blocks][2]
+    double *partials;       // [blocks][3]
     const double *gpart;    // epoch partial g-sums
 };
 
@@ -296,30 +307,36 @@ struct ValueParams {
 // quad*w = view - lin, i.e. (lin.u + u.u/2)/quad for u = view - lin
 // (LocalSubproblem.value_given_w, solver.py:132-135).  The g-sum of an
 // attempt comes from the epoch kernel's block partials; G(0) sums g(base).
+// Chunked mode (pipeline.py:158-197): the g-sum of an attempt over chunk c is
+// the accepted total minus the chunk's accepted share (mode 2) plus the
+// chunk's new share; an accepted chunk pass ends the chunk.
 __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
     SolveState *st = p.st;
-    if (st->done) return;
-    __shared__ double sm[64];
+    if (skip_attempt(st, p.seq)) return;
+    __shared__ double sm[96];
     __shared__ int s_last;
     const double *V = st->vw ? p.view1 : p.view0;
-    double acc[2] = {0.0, 0.0};
+    double acc[3] = {0.0, 0.0, 0.0};   // g-sum | view terms | non-finite count
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    if (p.mode) {
+    if (p.mode == 1 || (p.mode == 0 && p.view_terms)) {
         for (int64_t r = tid; r < p.d; r += nth) {
             const double v = V[r], l = p.lin[r];
-            if (!isfinite(v)) acc[1] += 1.0;
+            if (!isfinite(v)) acc[2] += 1.0;
             const double u = v - l;
-            acc[0] += l * u + 0.5 * u * u;
+            acc[1] += l * u + 0.5 * u * u;
         }
-    } else {
-        for (int64_t j = tid; j < p.m; j += nth)
-            acc[0] += g_one(p.kind, p.lam, p.rho, p.y ? p.y[j] : 0.0, p.base[j]);
     }
-    block_sum<2>(acc, sm);
+    if (p.mode != 1) {
+        for (int64_t j = tid; j < p.m; j += nth)
+            acc[0] += g_one(p.kind, p.lam, p.rho, p.y ? p.y[j] : 0.0,
+                            p.dfull ? p.base[j] + p.dfull[j] : p.base[j]);
+    }
+    block_sum<3>(acc, sm);
     if (threadIdx.x == 0) {
-        p.partials[blockIdx.x * 2 + 0] = acc[0];
-        p.partials[blockIdx.x * 2 + 1] = acc[1];
+        p.partials[blockIdx.x * 3 + 0] = acc[0];
+        p.partials[blockIdx.x * 3 + 1] = acc[1];
+        p.partials[blockIdx.x * 3 + 2] = acc[2];
         __threadfence();
         const unsigned ticket = atomicAdd(&st->block_counter, 1u);
         s_last = ticket == gridDim.x - 1;
@@ -327,31 +344,38 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double tot[2] = {0.0, 0.0};
+    double tot[3] = {0.0, 0.0, 0.0};
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-        tot[0] += __ldcg(p.partials + b * 2 + 0);
-        tot[1] += __ldcg(p.partials + b * 2 + 1);
+        tot[0] += __ldcg(p.partials + b * 3 + 0);
+        tot[1] += __ldcg(p.partials + b * 3 + 1);
+        tot[2] += __ldcg(p.partials + b * 3 + 2);
     }
     double gs[1] = {0.0};
-    if (p.mode) {
+    if (p.mode == 1) {
         const int eb = st->epoch_blocks;
         for (int b = threadIdx.x; b < eb; b += blockDim.x) gs[0] += __ldcg(p.gpart + b);
     }
-    block_sum<2>(tot, sm);
+    block_sum<3>(tot, sm);
     block_sum<1>(gs, sm);
     if (threadIdx.x != 0) return;
     st->block_counter = 0;
-    if (!p.mode) {
-        const double G0 = *p.cnst + tot[0];
+    if (p.mode == 2) {
+        st->gsum_old = tot[0];
+        return;
+    }
+    if (p.mode == 0) {
+        const double G0 = *p.cnst + (p.view_terms ? tot[1] / p.quad : 0.0) + tot[0];
         st->value = G0;
         st->initial = G0;
         st->gsum_acc = tot[0];
         return;
     }
-    const double G = *p.cnst + tot[0] / p.quad + gs[0];
-    // damped_solve control flow (solver.py:272-298)
+    const double gnew = p.chunked ? (st->gsum_acc - st->gsum_old) + gs[0] : gs[0];
+    const double G = *p.cnst + tot[1] / p.quad + gnew;
+    // damped_solve control flow (solver.py:272-298); per chunk: _train_chunk
+    // (pipeline.py:180-193)
     st->attempts += 1;
-    if (tot[1] > 0.0) {            // solver.py:279-280
+    if (tot[2] > 0.0) {            // solver.py:279-280
         st->status = GLM_SOLVER_ERROR;
         st->done = 1;
         return;
@@ -377,9 +401,9 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
         return;
     }
     st->value = G;
-    st->gsum_acc = gs[0];
+    st->gsum_acc = gnew;
     st->dc = st->dc == 0 ? 1 : 0;  // the buffer the epoch wrote
-    if (st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
+    if (!p.chunked && st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
     st->epochs_run += 1;
     if (st->epochs_run >= st->epochs_target) st->done = 1;
 }
@@ -420,8 +444,9 @@ __global__ void begin_kernel(SolveState *st, double *view0, double *view1, const
     }
 }
 
-__global__ void snapshot_kernel(const SolveState *st, double *view0, double *view1, int64_t d) {
-    if (st->done) return;
+__global__ void snapshot_kernel(const SolveState *st, double *view0, double *view1, int64_t d,
+                                int64_t seq) {
+    if (skip_attempt(st, seq)) return;
     const double *src = st->vw ? view1 : view0;
     double *dst = st->vw ? view0 : view1;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,6 +488,12 @@ __global__ void empty_solve_kernel(SolveState *st) {
     for (int i = 0; i < st->epochs_target && i < MAX_EPOCH_VALUES; ++i)
         st->epoch_values[i] = st->value;
     st->epochs_run = st->epochs_target;
+    st->done = 1;
+}
+
+__global__ void empty_chunk_kernel(SolveState *st, int64_t seq) {
+    if (st->seq != seq || st->done) return;
+    st->epochs_run = 1;
     st->done = 1;
 }
 
@@ -652,8 +683,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     ep.perm = s->perm;
     ep.gpart = s->gpart;
     ep.nnz = A->nnz;
+    ep.seq = -1;
 
-    ValueParams vp;
+    ValueParams vp{};
     vp.st = s->st;
     vp.kind = a->kind;
     vp.lam = a->lam;
@@ -669,6 +701,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     vp.view1 = s->view[1];
     vp.partials = s->partials;
     vp.gpart = s->gpart;
+    vp.seq = -1;
 
     const double avg = dense ? (double)d : (m > 0 ? (double)A->nnz / (double)m : 0.0);
     const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg);
@@ -723,7 +756,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
             count_launch();
             snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0],
-                                                                       s->view[1], d);
+                                                                       s->view[1], d, -1);
         }
         count_launch();
         if (a->mode == GLM_MODE_SEQUENTIAL) {
@@ -792,6 +825,234 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         s->prefetch_m = m;
     }
     if (res) return read_result(s, res, nullptr, 0, stream);
+    return GLM_OK;
+}
+
+// ------------------------------------------------- chunked (out-of-core)
+// The per-chunk damped pass of the streaming pipeline (_train_chunk,
+// pipeline.py:158-193) on the same kernels: chunk `seq` is opened only once
+// chunk seq-1 has finished (so the host may enqueue chunk seq+1 before it
+// has checked chunk seq), every attempt kernel is guarded by the open
+// sequence number, and the close kernel commits the accepted pass into the
+// partition-wide delta and reports to host-mapped memory.
+
+__global__ void stream_begin_kernel(SolveState *st, double *view0, double *view1,
+                                    const double *lin, int64_t d, double *dfull, int64_t m,
+                                    int zero_delta, int keep_view, double damping) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = tid; r < d; r += nth) {
+        const double v = keep_view ? view0[r] : lin[r];
+        view0[r] = v;
+        view1[r] = v;
+    }
+    if (zero_delta)
+        for (int64_t j = tid; j < m; j += nth) dfull[j] = 0.0;
+    if (tid == 0) {
+        st->damping = damping;
+        st->status = GLM_OK;
+        st->done = 0;
+        st->seq = -1;
+        st->dc = 0;
+        st->vw = 0;
+        st->block_counter = 0;
+        st->epoch_blocks = 0;
+        st->retries = 0;
+        st->attempts = 0;
+        st->plateaued = 0;
+        st->epochs_run = 0;
+        st->epochs_target = 1;
+    }
+}
+
+__global__ void chunk_open_kernel(SolveState *st, int64_t seq) {
+    if (st->status != GLM_OK || st->seq == seq) return;
+    if (st->seq != seq - 1 || (seq > 0 && !st->done)) return;   // previous chunk unfinished
+    st->seq = seq;
+    st->done = 0;
+    st->dc = 0;
+    st->plateaued = 0;
+    st->epochs_run = 0;
+    st->epochs_target = 1;
+    st->block_counter = 0;
+}
+
+__global__ void chunk_close_kernel(SolveState *st, int64_t seq, const double *dwork,
+                                   double *dfull, int64_t nc, ChunkRecord *rec) {
+    const bool mine = st->seq == seq;
+    if (mine && st->done && st->dc == 1) {     // an accepted pass: commit it
+        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t j = tid; j < nc; j += nth) dfull[j] = dwork[j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        volatile ChunkRecord *r = rec;
+        r->cur = st->seq;
+        r->done = mine ? st->done : 0;
+        r->status = st->status;
+        r->retries = st->retries;
+        r->attempts = st->attempts;
+        r->plateaued = mine ? st->plateaued : 0;
+        r->accepted = mine ? st->dc : 0;
+        r->damping = st->damping;
+        r->value = st->value;
+        __threadfence_system();
+        r->seq = seq;
+        __threadfence_system();
+    }
+}
+
+int stream_begin(glm_solver *s, const StreamSolve &a, bool zero_delta, bool keep_view,
+                 double damping, cudaStream_t stream) {
+    int rc = join_prefetch(s, stream);
+    if (rc) return rc;
+    count_launch();
+    stream_begin_kernel<<<grid_stride_blocks(a.d > a.m ? a.d : a.m), 256, 0, stream>>>(
+        s->st, s->view[0], s->view[1], a.lin, a.d, a.dfull, a.m, zero_delta ? 1 : 0,
+        keep_view ? 1 : 0, damping);
+    GLM_CUDA_TRY(cudaGetLastError());
+    ValueParams vp{};
+    vp.st = s->st;
+    vp.mode = 0;
+    vp.kind = a.kind;
+    vp.lam = a.lam;
+    vp.rho = a.rho;
+    vp.quad = a.quad;
+    vp.cnst = a.cnst;
+    vp.m = a.m;
+    vp.d = a.d;
+    vp.lin = a.lin;
+    vp.base = a.base;
+    vp.y = a.y;
+    vp.dfull = zero_delta ? nullptr : a.dfull;
+    vp.view_terms = keep_view ? 1 : 0;
+    vp.seq = -1;
+    vp.view0 = s->view[0];
+    vp.view1 = s->view[1];
+    vp.partials = s->partials;
+    vp.gpart = s->gpart;
+    int64_t n = a.m > a.d ? a.m : a.d;
+    int64_t b = (n + VALUE_THREADS - 1) / VALUE_THREADS;
+    b = b < 1 ? 1 : (b > VALUE_MAX_BLOCKS ? VALUE_MAX_BLOCKS : b);
+    count_launch();
+    value_kernel<<<(int)b, VALUE_THREADS, 0, stream>>>(vp);
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+int chunk_enqueue(glm_solver *s, const StreamSolve &a, const ChunkJob &c, cudaStream_t stream) {
+    const glm_matrix *A = c.A;
+    const int64_t nc = A->n_cols, d = A->n_rows;
+    if (nc > s->max_coords || d > s->max_rows)
+        return glm_set_error(GLM_USAGE, "chunk larger than the stream solver");
+    int rc = ensure_device_tables();
+    if (rc) return rc;
+    if (c.gen_perm && nc > 0) {
+        const PermScratch ps = carve_perm_scratch(s->perm_mem, s->max_coords, nc);
+        rc = chunk_perm(c.key_seed, nc, c.perm, ps, stream);
+        if (rc) return rc;
+    }
+    if (c.open) {
+        count_launch();
+        chunk_open_kernel<<<1, 1, 0, stream>>>(s->st, c.seq);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
+    ValueParams vp{};
+    vp.st = s->st;
+    vp.kind = a.kind;
+    vp.lam = a.lam;
+    vp.rho = a.rho;
+    vp.quad = a.quad;
+    vp.cnst = a.cnst;
+    vp.lin = a.lin;
+    vp.seq = c.seq;
+    vp.view0 = s->view[0];
+    vp.view1 = s->view[1];
+    vp.partials = s->partials;
+    vp.gpart = s->gpart;
+    auto grid_of = [](int64_t n) {
+        int64_t b = (n + VALUE_THREADS - 1) / VALUE_THREADS;
+        return (int)(b < 1 ? 1 : (b > VALUE_MAX_BLOCKS ? VALUE_MAX_BLOCKS : b));
+    };
+    if (c.open) {   // the chunk's g-sum in the accepted state (mode 2)
+        vp.mode = 2;
+        vp.m = nc;
+        vp.d = 0;
+        vp.base = a.base + c.lo;
+        vp.y = a.y ? a.y + c.lo : nullptr;
+        vp.dfull = a.dfull + c.lo;
+        count_launch();
+        value_kernel<<<grid_of(nc), VALUE_THREADS, 0, stream>>>(vp);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
+    EpochParams ep{};
+    ep.st = s->st;
+    ep.kind = a.kind;
+    ep.lam = a.lam;
+    ep.rho = a.rho;
+    ep.quad = a.quad;
+    ep.m = nc;
+    ep.d = d;
+    ep.indptr = A->indptr;
+    ep.rows = A->rows;
+    ep.vals = A->vals;
+    ep.sq = A->sqnorms;
+    ep.base = a.base + c.lo;
+    ep.y = a.y ? a.y + c.lo : nullptr;
+    ep.delta0 = a.dfull + c.lo;     // read: the accepted state (st->dc == 0)
+    ep.delta1 = s->delta[1];        // written: the attempt
+    ep.view0 = s->view[0];
+    ep.view1 = s->view[1];
+    ep.perm = c.perm;
+    ep.gpart = s->gpart;
+    ep.nnz = A->nnz;
+    ep.seq = c.seq;
+    vp.mode = 1;
+    vp.chunked = 1;
+    vp.m = nc;
+    vp.d = d;
+    vp.base = nullptr;
+    vp.y = nullptr;
+    vp.dfull = nullptr;
+    const bool dense = A->layout == GLM_DENSE;
+    const double avg = dense ? (double)d : (nc > 0 ? (double)A->nnz / (double)nc : 0.0);
+    const int lanes = a.group_lanes > 0 ? a.group_lanes : auto_lanes(avg);
+    for (int i = 0; i < c.attempts && nc > 0; ++i) {
+        count_launch();
+        snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1],
+                                                                   d, c.seq);
+        count_launch();
+        if (a.mode == GLM_MODE_SEQUENTIAL) {
+            const bool small = avg <= 96.0;
+            if (dense) rc = small ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
+            else rc = small ? launch_seq_t<32, false>(ep, stream) : launch_seq_t<256, false>(ep, stream);
+        } else {
+            rc = dense ? launch_async<true>(ep, lanes, a.max_inflight, a.flags, stream)
+                       : launch_async<false>(ep, lanes, a.max_inflight, a.flags, stream);
+        }
+        if (rc) return rc;
+        count_launch();
+        value_kernel<<<grid_of(d), VALUE_THREADS, 0, stream>>>(vp);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
+    if (nc == 0 && c.open) {   // an empty chunk is one accepted no-op pass
+        count_launch();
+        empty_chunk_kernel<<<1, 1, 0, stream>>>(s->st, c.seq);
+    }
+    count_launch();
+    chunk_close_kernel<<<grid_stride_blocks(nc), 256, 0, stream>>>(s->st, c.seq, s->delta[1],
+                                                                   a.dfull + c.lo, nc, c.rec);
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+int stream_finalize(glm_solver *s, const StreamSolve &a, double *dv_out, cudaStream_t stream) {
+    if (!dv_out) return GLM_OK;
+    count_launch();
+    finalize_kernel<<<grid_stride_blocks(a.d), 256, 0, stream>>>(
+        s->st, nullptr, nullptr, s->view[0], s->view[1], a.lin, a.quad, 0, a.d, nullptr, dv_out,
+        0);
+    GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
 

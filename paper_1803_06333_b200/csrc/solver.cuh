@@ -41,4 +41,40 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
 int join_prefetch(glm_solver *s, cudaStream_t stream);
 
+// ---- chunked (out-of-core) solves: stream.cu drives these per chunk.
+struct ChunkRecord {          // written by the close kernel into host-mapped memory
+    int64_t seq;              // chunk sequence number this record answers (written last)
+    int64_t cur;              // chunk open on the device when written
+    int32_t done, status, retries, attempts, plateaued, accepted;
+    double damping, value;
+};
+
+struct StreamSolve {          // partition-wide arguments (device pointers)
+    int kind, mode;
+    double lam, rho, quad;
+    const double *cnst;       // device scalar
+    const double *lin;        // f64[d]
+    const double *base;       // f64[m]
+    const double *y;          // f64[m] or null
+    double *dfull;            // f64[m] partition delta (accepted state)
+    int64_t m, d;
+    int group_lanes, max_inflight, flags;
+};
+
+struct ChunkJob {
+    const glm_matrix *A;      // chunk matrix (columns lo .. lo + n_cols of the partition)
+    int64_t lo;
+    int64_t seq;              // epoch * n_chunks + chunk
+    uint64_t key_seed;        // derive_seed(seed, epoch_index, chunk) (pipeline.py:226-227)
+    int32_t *perm;
+    bool gen_perm, open;
+    int attempts;
+    ChunkRecord *rec;         // host-mapped
+};
+
+int stream_begin(glm_solver *s, const StreamSolve &a, bool zero_delta, bool keep_view,
+                 double damping, cudaStream_t stream);
+int chunk_enqueue(glm_solver *s, const StreamSolve &a, const ChunkJob &c, cudaStream_t stream);
+int stream_finalize(glm_solver *s, const StreamSolve &a, double *dv_out, cudaStream_t stream);
+
 }  // namespace glm
