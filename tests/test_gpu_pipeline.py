@@ -88,10 +88,10 @@ def test_streamed_equals_resident_bits_host_and_file(tmp_path):
     store = g.open_chunks(tmp_path / "s.chunks")
     outs = []
     for src, budget, pin in [("host", None, False), ("host", 1, False), ("host", 1, True),
-                             ("file", 1, False), ("file", 200_000, False)]:
+                             ("file", 1, False), ("file", 600_000, False)]:
         part = P.StreamingPartition(store if src == "file" else m, chunk_size=1_000,
                                     device_budget=budget, pin_host=pin)
-        if budget == 200_000:
+        if budget == 600_000:
             assert 0 < part.n_resident < part.n_chunks      # resident prefix + streaming
         runner = P.chunked_device_runner(part, seed=5, epochs=3)
         res = _train(m, spec, runner, 2, 3, 5)
