@@ -202,6 +202,184 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     store_block_gsum(gacc, p.gpart, st);
 }
 
+
+// ------------------------------------------------------ narrow dense
+// Dense columns with d <= 32*R rows (C3: HIGGS-shaped, d = 28).  Lane l of a
+// warp owns rows l, l+32, ... of the column and of the view, so a coordinate
+// is R coalesced loads, R FMAs, one butterfly all-reduce (every lane ends
+// with the same bits, so every lane takes the same step) and R FMAs — no
+// shared-vector traffic on the critical path.  The next coordinate's column
+// and metadata are loaded while the current one is stepped.
+
+template <int R>
+struct NarrowCol {
+    double a[R];
+    double b, dj, s, y;
+    int j;
+};
+
+template <int R>
+__device__ __forceinline__ void narrow_load(const EpochParams &p, const double *dcur, int64_t k,
+                                            NarrowCol<R> &c) {
+    const int lane = threadIdx.x & 31;
+    const int j = __ldg(p.perm + k);
+    c.j = j;
+    const double *col = p.vals + (int64_t)j * p.d;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        c.a[i] = r < p.d ? __ldg(col + r) : 0.0;
+    }
+    c.b = __ldg(p.base + j);
+    c.dj = dcur ? dcur[j] : 0.0;
+    c.s = __ldg(p.sq + j);
+    c.y = p.y ? __ldg(p.y + j) : 0.0;
+}
+
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic mode (run_pass n_threads=1, solver.py:202-211): one warp, the
+// view in registers.
+template <int R>
+__global__ void __launch_bounds__(32) scd_seq_narrow(EpochParams p) {
+    SolveState *st = p.st;
+    if (skip_attempt(st, p.seq)) return;
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
+    double *view = st->vw ? p.view1 : p.view0;
+    const int lane = threadIdx.x;
+    double v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        v[i] = r < p.d ? view[r] : 0.0;
+    }
+    const int kind = p.kind;
+    double gacc = 0.0;
+    NarrowCol<R> nx;
+    if (p.m > 0) narrow_load<R>(p, dcur, 0, nx);
+    for (int64_t k = 0; k < p.m; ++k) {
+        const NarrowCol<R> c = nx;
+        if (k + 1 < p.m) narrow_load<R>(p, dcur, k + 1, nx);
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc += c.a[i] * v[i];
+        const double ga = warp_allsum(acc);
+        double raw = 0.0;
+        if (!coord_step(kind, p.lam, p.rho, c.y, ga, p.quad * c.s, c.b + c.dj, raw)) {
+            if (lane == 0) flag_error(st);
+            raw = 0.0;
+        }
+        const double step = damping * raw;
+        const double dn = step != 0.0 ? c.dj + step : c.dj;
+        if (lane == 0) {
+            dnext[c.j] = dn;
+            gacc += g_one(kind, p.lam, p.rho, c.y, c.b + dn);
+        }
+        if (step != 0.0) {
+            const double f = p.quad * step;
+#pragma unroll
+            for (int i = 0; i < R; ++i) v[i] += f * c.a[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        if (r < p.d) view[r] = v[i];
+    }
+    if (lane == 0) {
+        p.gpart[0] = gacc;
+        st->epoch_blocks = 1;
+    }
+}
+
+// Asynchronous mode (TPA-SCD) for narrow dense data: a global red.add per
+// row per coordinate would serialise every coordinate on the same d L2
+// addresses, so each warp keeps its own pending Delta view in registers and
+// reads view = (CTA snapshot of the shared view) + (its own pending).  Every
+// `per_phase` coordinates per warp the CTA folds the warps' pendings, adds
+// them to the shared view with one atom.add per row, and refreshes its
+// snapshot from the values the atomics returned.  Staleness is bounded by
+// grid x warps x per_phase coordinates (the in-flight budget); the damping
+// check of the value kernel guards the epoch as for scd_async.
+template <int R>
+__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase) {
+    SolveState *st = p.st;
+    if (skip_attempt(st, p.seq)) return;
+    __shared__ double snap[32 * R];
+    __shared__ double fold[32 * R];
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
+    double *view = st->vw ? p.view1 : p.view0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarp = blockDim.x >> 5;
+    for (int r = threadIdx.x; r < 32 * R; r += blockDim.x) {
+        snap[r] = r < p.d ? ld_cg(view + r) : 0.0;
+        fold[r] = 0.0;
+    }
+    __syncthreads();
+    const int kind = p.kind;
+    double gacc = 0.0;
+    double pend[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) pend[i] = 0.0;
+    const int64_t per_cta = (int64_t)nwarp * per_phase;
+    for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m;
+         k0 += (int64_t)gridDim.x * per_cta) {
+        const int64_t kb = k0 + (int64_t)warp * per_phase;
+        const int64_t ke = min(kb + per_phase, p.m);
+        NarrowCol<R> nx;
+        if (kb < ke) narrow_load<R>(p, dcur, kb, nx);
+        for (int64_t k = kb; k < ke; ++k) {
+            const NarrowCol<R> c = nx;
+            if (k + 1 < ke) narrow_load<R>(p, dcur, k + 1, nx);
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) acc += c.a[i] * (snap[lane + 32 * i] + pend[i]);
+            const double ga = warp_allsum(acc);
+            double raw = 0.0;
+            if (!coord_step(kind, p.lam, p.rho, c.y, ga, p.quad * c.s, c.b + c.dj, raw)) {
+                if (lane == 0) flag_error(st);
+                raw = 0.0;
+            }
+            const double step = damping * raw;
+            const double dn = step != 0.0 ? c.dj + step : c.dj;
+            if (lane == 0) {
+                dnext[c.j] = dn;
+                gacc += g_one(kind, p.lam, p.rho, c.y, c.b + dn);
+            }
+            if (step != 0.0) {
+                const double f = p.quad * step;
+#pragma unroll
+                for (int i = 0; i < R; ++i) pend[i] += f * c.a[i];
+            }
+        }
+        // phase end: fold the warps' pendings, publish, refresh the snapshot
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (pend[i] != 0.0) atomicAdd(&fold[lane + 32 * i], pend[i]);
+        __syncthreads();
+        for (int r = threadIdx.x; r < p.d; r += blockDim.x) {
+            const double x = fold[r];
+            const double old = atomicAdd(view + r, x);
+            snap[r] = old + x;
+            fold[r] = 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) pend[i] = 0.0;
+        __syncthreads();
+    }
+    store_block_gsum(gacc, p.gpart, st);
+}
+
 // ----------------------------------------------------------- sequential
 // One CTA of BS threads walks the permutation in order (run_pass with
 // n_threads=1, solver.py:202-211).  Deterministic: fixed per-thread strides
@@ -562,6 +740,94 @@ static int launch_async(const EpochParams &p, int lanes, int max_inflight, int f
     }
 }
 
+
+// Narrow dense launch: R = rows per lane.  The async grid follows the
+// in-flight budget: warps x per_phase x CTAs <= budget (budget 0 = auto:
+// 32 * d / nnz-per-column / (quad * mean |a|^2), the coupling-scaled
+// feature-conflict budget; at least one warp per SM).
+static int narrow_rows(int64_t d) {
+    if (d <= 32) return 1;
+    if (d <= 64) return 2;
+    if (d <= 128) return 4;
+    if (d <= 256) return 8;
+    return 0;
+}
+
+template <int R>
+static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, cudaStream_t s) {
+    count_launch();
+    if (!async) {
+        scd_seq_narrow<R><<<1, 32, 0, s>>>(p);
+    } else {
+        static int blocks_per_sm = 0;
+        if (!blocks_per_sm) {
+            GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                                       scd_replica<R>, 256, 0));
+            if (blocks_per_sm < 1) blocks_per_sm = 1;
+        }
+        constexpr int W = 8;
+        int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
+        if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
+        int64_t grid = budget / W;
+        if (grid < 1) grid = 1;
+        if (grid > cap) grid = cap;
+        const int64_t need = (p.m + W - 1) / W;      // at least one coordinate per warp
+        if (grid > need) grid = need < 1 ? 1 : need;
+        int64_t per = budget / (grid * W);
+        if (per < 1) per = 1;
+        if (per > 64) per = 64;
+        scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per);
+    }
+    GLM_CUDA_TRY(cudaGetLastError());
+    return GLM_OK;
+}
+
+static int launch_narrow(const EpochParams &p, bool async, int64_t budget, cudaStream_t s) {
+    switch (narrow_rows(p.d)) {
+    case 1: return launch_narrow_t<1>(p, async, budget, s);
+    case 2: return launch_narrow_t<2>(p, async, budget, s);
+    case 4: return launch_narrow_t<4>(p, async, budget, s);
+    default: return launch_narrow_t<8>(p, async, budget, s);
+    }
+}
+
+__global__ void mean_kernel(const double *x, int64_t n, double *out) {
+    __shared__ double sm[32];
+    double acc[1] = {0.0};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc[0] += x[i];
+    block_sum<1>(acc, sm);
+    if (threadIdx.x == 0) out[0] = n > 0 ? acc[0] / (double)n : 1.0;
+}
+
+// mean |a_j|^2 of a partition (cached per sqnorm array; one sync the first time)
+static int mean_sqnorm(glm_solver *s, const double *sq, int64_t m, cudaStream_t stream,
+                       double *out) {
+    if (s->sq_src == sq && s->sq_n == m) {
+        *out = s->sq_mean;
+        return GLM_OK;
+    }
+    count_launch();
+    mean_kernel<<<1, 1024, 0, stream>>>(sq, m, s->scratch);
+    GLM_CUDA_TRY(cudaGetLastError());
+    double h = 1.0;
+    GLM_CUDA_TRY(cudaMemcpyAsync(&h, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    GLM_CUDA_TRY(cudaStreamSynchronize(stream));
+    s->sq_src = sq;
+    s->sq_n = m;
+    s->sq_mean = h > 0.0 ? h : 1.0;
+    *out = s->sq_mean;
+    return GLM_OK;
+}
+
+static int64_t narrow_budget(const EpochParams &p, double sq_mean, int max_inflight) {
+    if (max_inflight > 0) return max_inflight;
+    const double c = p.quad * sq_mean;
+    double b = 32.0 / (c > 1e-300 ? c : 1e-300);
+    if (b < 32.0) b = 32.0;
+    if (b > 1e9) b = 1e9;
+    return (int64_t)b;
+}
+
 constexpr int64_t SMEM_VIEW_MAX = 24 * 1024;   // doubles (192 KB)
 
 template <int BS, bool DENSE>
@@ -713,6 +979,13 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         return (int)b;
     };
 
+    const bool narrow = dense && narrow_rows(d) > 0;
+    int64_t nbudget = 0;
+    if (narrow && a->mode != GLM_MODE_SEQUENTIAL && m > 0) {
+        double sqm = 1.0;
+        if ((rc = mean_sqnorm(s, A->sqnorms, m, stream, &sqm))) return rc;
+        nbudget = narrow_budget(ep, sqm, a->max_inflight);
+    }
     const int reuse = (a->flags & GLM_FLAG_REUSE_GSUM) ? 1 : 0;
     count_launch();
     begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1], a->lin,
@@ -758,8 +1031,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0],
                                                                        s->view[1], d, -1);
         }
-        count_launch();
-        if (a->mode == GLM_MODE_SEQUENTIAL) {
+        if (narrow) {
+            r = launch_narrow(ep, a->mode != GLM_MODE_SEQUENTIAL, nbudget, stream);
+        } else if (a->mode == GLM_MODE_SEQUENTIAL) {
             if (dense) r = seq_bs == 32 ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
             else r = seq_bs == 32 ? launch_seq_t<32, false>(ep, stream) : launch_seq_t<256, false>(ep, stream);
         } else {
@@ -1021,7 +1295,6 @@ int chunk_enqueue(glm_solver *s, const StreamSolve &a, const ChunkJob &c, cudaSt
         count_launch();
         snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1],
                                                                    d, c.seq);
-        count_launch();
         if (a.mode == GLM_MODE_SEQUENTIAL) {
             const bool small = avg <= 96.0;
             if (dense) rc = small ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);

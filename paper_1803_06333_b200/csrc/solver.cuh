@@ -27,6 +27,9 @@ struct glm_solver {
     std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
     int last_epochs = 0;
     int64_t last_m = 0;
+    const double *sq_src = nullptr;       // mean |a|^2 cache (narrow dense budget)
+    int64_t sq_n = -1;
+    double sq_mean = 1.0;
 };
 
 namespace glm {

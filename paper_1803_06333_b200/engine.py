@@ -99,6 +99,9 @@ class ConvergenceTrace:
     def objectives(self):
         return np.array([r.objective for r in self.rows])
 
+    def gaps(self):
+        return np.array([np.nan if r.gap is None else r.gap for r in self.rows])
+
     def write_csv(self, path):
         with open(path, "w") as fh:
             fh.write(self.HEADER + "\n")
