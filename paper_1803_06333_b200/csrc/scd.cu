@@ -636,7 +636,7 @@ __global__ void snapshot_kernel(const SolveState *st, double *view0, double *vie
 __global__ void finalize_kernel(SolveState *st, const double *delta0, const double *delta1,
                                 const double *view0, const double *view1, const double *lin,
                                 double quad, int64_t m, int64_t d, double *delta_out,
-                                double *dv_out, int accumulate) {
+                                double *dv_out, int accumulate, int box) {
     const int dc = st->dc;
     const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
     const double *V = st->vw ? view1 : view0;
@@ -644,7 +644,14 @@ __global__ void finalize_kernel(SolveState *st, const double *delta0, const doub
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if (delta_out) {
         if (accumulate) {
-            if (dl)
+            // folding into alpha: a coordinate clipped to a bound of the SVM box
+            // lands there up to the rounding of base + delta (the reference can
+            // step an ulp outside and then fails its own check_alpha,
+            // objectives.py:110-112); keep the folded alpha in the box
+            if (dl && box)
+                for (int64_t j = tid; j < m; j += nth)
+                    delta_out[j] = fmin(1.0, fmax(0.0, delta_out[j] + dl[j]));
+            else if (dl)
                 for (int64_t j = tid; j < m; j += nth) delta_out[j] += dl[j];
         } else {
             for (int64_t j = tid; j < m; j += nth) delta_out[j] = dl ? dl[j] : 0.0;
@@ -1078,7 +1085,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     count_launch();
     finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
-        delta_out, dv_out, a->accumulate);
+        delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0);
     GLM_CUDA_TRY(cudaGetLastError());
     s->last_epochs = a->epochs;
     s->last_m = m;
@@ -1324,7 +1331,7 @@ int stream_finalize(glm_solver *s, const StreamSolve &a, double *dv_out, cudaStr
     count_launch();
     finalize_kernel<<<grid_stride_blocks(a.d), 256, 0, stream>>>(
         s->st, nullptr, nullptr, s->view[0], s->view[1], a.lin, a.quad, 0, a.d, nullptr, dv_out,
-        0);
+        0, 0);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }

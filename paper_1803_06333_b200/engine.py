@@ -348,6 +348,8 @@ class Engine:
                                   base=a_slice.clone(), data=wk.data, col_ids=wk.cols)
             res = self.chunk_runner(sub, wk, cfg)
             a_slice += D.to_device(res.delta_alpha)
+            if self.spec.kind == "dual_l2_svm":     # keep the fold in the box (scd.cu finalize)
+                a_slice.clamp_(0.0, 1.0)
             vbar[:self.d] += D.to_device(res.delta_v)
             wk.last = res
             return
