@@ -134,6 +134,7 @@ int glm_solver_destroy(glm_solver *s) {
     cudaFree(s->partials);
     cudaFree(s->gpart);
     cudaFree(s->scratch);
+    cudaFree(s->vpad);
     if (s->side) {
         cudaStreamSynchronize(s->side);
         cudaStreamDestroy(s->side);
@@ -174,6 +175,7 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     chk(cudaMalloc(&s->partials, sizeof(double) * 3 * 8 * NUM_SMS));
     chk(cudaMalloc(&s->gpart, sizeof(double) * 16 * NUM_SMS));
     chk(cudaMalloc(&s->scratch, REDUCE_SCRATCH_BYTES));
+    chk(cudaMalloc(&s->vpad, sizeof(double) * 256 * 128));
     if (e == cudaSuccess) {
         chk(cudaMemset(s->perm_mem, 0, pb));
         chk(cudaMemset(s->scratch, 0, REDUCE_SCRATCH_BYTES));

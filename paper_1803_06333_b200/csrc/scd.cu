@@ -308,12 +308,26 @@ __global__ void __launch_bounds__(32) scd_seq_narrow(EpochParams p) {
 // snapshot from the values the atomics returned.  Staleness is bounded by
 // grid x warps x per_phase coordinates (the in-flight budget); the damping
 // check of the value kernel guards the epoch as for scd_async.
+// The shared view lives, for the kernel's duration, in `vpad` with one row
+// per 1 KB (PAD_STRIDE doubles) so the d rows hash to d different L2 slices
+// (address bits 10+); contiguous, all CTAs' atomics would queue on the one
+// or two slices holding the view's 224 bytes.
+constexpr int PAD_STRIDE = 128;
+
+__global__ void narrow_pad_kernel(const SolveState *st, const double *view0, const double *view1,
+                                  double *vpad, int64_t d, int64_t seq) {
+    if (skip_attempt(st, seq)) return;
+    const double *view = st->vw ? view1 : view0;
+    for (int64_t r = threadIdx.x; r < d; r += blockDim.x) vpad[r * PAD_STRIDE] = view[r];
+}
+
 template <int R>
-__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase) {
+__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase, double *vpad) {
     SolveState *st = p.st;
     if (skip_attempt(st, p.seq)) return;
     __shared__ double snap[32 * R];
     __shared__ double fold[32 * R];
+    __shared__ int s_last;
     const int dc = st->dc;
     const double damping = st->damping;
     const double *dcur = delta_cur(p, dc);
@@ -322,7 +336,7 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarp = blockDim.x >> 5;
     for (int r = threadIdx.x; r < 32 * R; r += blockDim.x) {
-        snap[r] = r < p.d ? ld_cg(view + r) : 0.0;
+        snap[r] = r < p.d ? ld_cg(vpad + (int64_t)r * PAD_STRIDE) : 0.0;
         fold[r] = 0.0;
     }
     __syncthreads();
@@ -332,15 +346,21 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase)
 #pragma unroll
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
     const int64_t per_cta = (int64_t)nwarp * per_phase;
-    for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m;
-         k0 += (int64_t)gridDim.x * per_cta) {
+    const int64_t stride = (int64_t)gridDim.x * per_cta;
+    NarrowCol<R> nx;
+    {
+        const int64_t kb0 = (int64_t)blockIdx.x * per_cta + (int64_t)warp * per_phase;
+        if (kb0 < p.m) narrow_load<R>(p, dcur, kb0, nx);
+    }
+    for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m; k0 += stride) {
         const int64_t kb = k0 + (int64_t)warp * per_phase;
         const int64_t ke = min(kb + per_phase, p.m);
-        NarrowCol<R> nx;
-        if (kb < ke) narrow_load<R>(p, dcur, kb, nx);
         for (int64_t k = kb; k < ke; ++k) {
             const NarrowCol<R> c = nx;
+            // prefetch the next coordinate of this warp, across the phase
+            // boundary too (the column stream never waits on the fold)
             if (k + 1 < ke) narrow_load<R>(p, dcur, k + 1, nx);
+            else if (kb + stride < p.m) narrow_load<R>(p, dcur, kb + stride, nx);
             double acc = 0.0;
 #pragma unroll
             for (int i = 0; i < R; ++i) acc += c.a[i] * (snap[lane + 32 * i] + pend[i]);
@@ -369,13 +389,26 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase)
         __syncthreads();
         for (int r = threadIdx.x; r < p.d; r += blockDim.x) {
             const double x = fold[r];
-            const double old = atomicAdd(view + r, x);
+            const double old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
             snap[r] = old + x;
             fold[r] = 0.0;
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) pend[i] = 0.0;
         __syncthreads();
+    }
+    // the last CTA to finish writes the shared view back
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&st->block_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int r = threadIdx.x; r < p.d; r += blockDim.x)
+            view[r] = ld_cg(vpad + (int64_t)r * PAD_STRIDE);
+        __syncthreads();
+        if (threadIdx.x == 0) st->block_counter = 0;
     }
     store_block_gsum(gacc, p.gpart, st);
 }
@@ -761,7 +794,8 @@ static int narrow_rows(int64_t d) {
 }
 
 template <int R>
-static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, cudaStream_t s) {
+static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, double *vpad,
+                           cudaStream_t s) {
     count_launch();
     if (!async) {
         scd_seq_narrow<R><<<1, 32, 0, s>>>(p);
@@ -783,18 +817,21 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, cud
         int64_t per = budget / (grid * W);
         if (per < 1) per = 1;
         if (per > 64) per = 64;
-        scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per);
+        narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
+        count_launch();
+        scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
     }
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
 
-static int launch_narrow(const EpochParams &p, bool async, int64_t budget, cudaStream_t s) {
+static int launch_narrow(const EpochParams &p, bool async, int64_t budget, double *vpad,
+                         cudaStream_t s) {
     switch (narrow_rows(p.d)) {
-    case 1: return launch_narrow_t<1>(p, async, budget, s);
-    case 2: return launch_narrow_t<2>(p, async, budget, s);
-    case 4: return launch_narrow_t<4>(p, async, budget, s);
-    default: return launch_narrow_t<8>(p, async, budget, s);
+    case 1: return launch_narrow_t<1>(p, async, budget, vpad, s);
+    case 2: return launch_narrow_t<2>(p, async, budget, vpad, s);
+    case 4: return launch_narrow_t<4>(p, async, budget, vpad, s);
+    default: return launch_narrow_t<8>(p, async, budget, vpad, s);
     }
 }
 
@@ -1039,7 +1076,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
                                                                        s->view[1], d, -1);
         }
         if (narrow) {
-            r = launch_narrow(ep, a->mode != GLM_MODE_SEQUENTIAL, nbudget, stream);
+            r = launch_narrow(ep, a->mode != GLM_MODE_SEQUENTIAL, nbudget, s->vpad, stream);
         } else if (a->mode == GLM_MODE_SEQUENTIAL) {
             if (dense) r = seq_bs == 32 ? launch_seq_t<32, true>(ep, stream) : launch_seq_t<256, true>(ep, stream);
             else r = seq_bs == 32 ? launch_seq_t<32, false>(ep, stream) : launch_seq_t<256, false>(ep, stream);

@@ -19,6 +19,7 @@ struct glm_solver {
     double *partials = nullptr;           // value-kernel block partials
     double *gpart = nullptr;              // epoch-kernel block partial g-sums
     double *scratch = nullptr;            // generic reduction scratch
+    double *vpad = nullptr;               // slice-spread view of the narrow async kernel
     int timing = 0;                       // record per-attempt CUDA events
     cudaStream_t side = nullptr;          // permutation prefetch stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
