@@ -149,7 +149,9 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import datetime
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=180))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -172,6 +174,22 @@ def load_ncu_traffic():
             return json.load(fh)
     except Exception:
         return None
+
+
+def l2_ceiling(nnz_loc, epoch_ms):
+    exe = os.path.join(ROOT, "tools", "l2_random_roofline")
+    try:
+        out = subprocess.run([exe, str(D_FEAT), str(nnz_loc)], capture_output=True, text=True,
+                             timeout=60).stdout
+        m = json.loads(out.strip().splitlines()[-1])
+    except Exception as exc:    # pragma: no cover - binary missing
+        return {"unavailable": repr(exc)}
+    return {"what": f"{nnz_loc} random ld.cg.f64 + {nnz_loc} random red.add.f64 into a "
+                    f"{D_FEAT}-double vector (the epoch's shared-vector traffic)",
+            "ceiling_ms": m["mixed_ms"], "epoch_kernel_ms": epoch_ms,
+            "frac": m["mixed_ms"] / epoch_ms, "gather_only_ms": m["gather_ms"],
+            "red_only_ms": m["red_ms"], "column_stream_480MB_ms": m["stream480MB_ms"],
+            "source": "tools/l2_random_roofline.cu, run live by bench.py"}
 
 
 # ------------------------------------------------------------ CPU arm
@@ -372,6 +390,13 @@ def ours_main(args):
                                       "epoch": epoch_ms,
                                       "value_damping": kern_ms[2] / max(attempts, 1),
                                       "step": ms_step}}
+    # The epoch's real ceiling: every nnz is one random 8-byte gather and one
+    # random f64 red into the L2-resident shared vector.  Measured live by a
+    # microbenchmark doing exactly the epoch's nnz_loc gathers + reds into a
+    # d-double vector (tools/l2_random_roofline.cu); frac > ~0.9 means the
+    # epoch kernel runs at the L2 random-access limit, not an HBM one.
+    if rank == 0:
+        roofline["l2_random_ceiling"] = l2_ceiling(nnz_loc, epoch_ms)
 
     phase("timed region done", rank)
     # -------- e2e through the reference-facing C-ABI with host buffers
@@ -414,10 +439,13 @@ def ours_main(args):
                                  "epochs_run_last_round": int(res_state.epochs_run),
                                  "damping": float(res_state.damping)}}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
-    return 0
+    # Every collective of this run has completed (the JSON line needed them all).
+    # Leave without the NCCL teardown: destroying a communicator that CUDA
+    # graphs captured can block the watchdog past the driver's limits.
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world):
@@ -467,6 +495,12 @@ def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world
 
 
 def main():
+    import faulthandler
+    # a multi-rank run that stops making progress dumps every thread's stack
+    # and exits instead of holding the box until the driver's limit
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        faulthandler.dump_traceback_later(float(os.environ.get("BENCH_HANG_S", "300")),
+                                          exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
@@ -478,7 +512,8 @@ def main():
     ap.add_argument("--graph", type=int, default=1, help="replay trajectories as CUDA graphs")
     ap.add_argument("--traj", type=int, default=20,
                     help="epochs per timed trajectory from alpha0")
-    ap.add_argument("--lanes", type=int, default=4, help="lanes per coordinate (tools/sweep_c2.py)")
+    ap.add_argument("--lanes", type=int, default=0,
+                    help="lanes per coordinate | registers << 8 (0 = auto; tools/sweep_c2.py)")
     ap.add_argument("--cache-flags", type=int, default=1, help="glm_solve_args.flags")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -759,11 +759,18 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     return GLM_OK;
 }
 
+// lanes = G | (R << 8): G lanes per coordinate holding R column elements
+// each in registers (R = 0: the default for G)
 template <bool DENSE, int CM>
 static int launch_async_cm(const EpochParams &p, int lanes, int max_inflight, cudaStream_t s) {
-    switch (lanes) {
-    case 4: return launch_async_t<4, 4, DENSE, CM>(p, max_inflight, s);
-    case 8: return launch_async_t<8, 8, DENSE, CM>(p, max_inflight, s);
+    const int G = lanes & 0xff, R = lanes >> 8;
+    switch (G) {
+    case 4:
+        if (R >= 10) return launch_async_t<4, 10, DENSE, CM>(p, max_inflight, s);
+        return launch_async_t<4, 4, DENSE, CM>(p, max_inflight, s);
+    case 8:
+        if (R > 0 && R <= 5) return launch_async_t<8, 5, DENSE, CM>(p, max_inflight, s);
+        return launch_async_t<8, 8, DENSE, CM>(p, max_inflight, s);
     case 16: return launch_async_t<16, 4, DENSE, CM>(p, max_inflight, s);
     default: return launch_async_t<32, 4, DENSE, CM>(p, max_inflight, s);
     }
@@ -893,6 +900,7 @@ static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
 
 static int auto_lanes(double avg_nnz) {   // lanes x registers cover the column
     if (avg_nnz <= 16) return 4;
+    if (avg_nnz <= 40) return 4 | (10 << 8);   // C2 / C5: 4 lanes x 10 registers (tools/sweep_c2.py)
     if (avg_nnz <= 64) return 8;
     return 32;
 }

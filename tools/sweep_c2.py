@@ -21,8 +21,9 @@ dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
 spec = g.ObjectiveSpec("dual_l2_logistic", bench.LAM, bench.N_EX, bench.D_FEAT)
 cfg = g.HierarchyConfig(t1=10 ** 6, seed=0, epochs=1)
 import itertools
-variants = [dict(group_lanes=l, cache_flags=c) for c, l in itertools.product((0, 1, 2, 3),
-                                                                           (4, 8, 16))]
+LANES = [int(x) for x in os.environ.get("SWEEP_LANES", "4,2564,1288,8").split(",")]
+CMS = [int(x) for x in os.environ.get("SWEEP_CM", "1").split(",")]
+variants = [dict(group_lanes=l, cache_flags=c) for c, l in itertools.product(CMS, LANES)]
 out = []
 for var in variants:
     eng = g.Engine(dm, spec, cfg, mode="async", sync_solves=False, retry_budget=0, **var)
