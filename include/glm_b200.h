@@ -74,6 +74,8 @@ typedef struct {
     const double *sqnorms;   /* f64[n_cols] (col_sqnorms, data.py:98-107) */
 } glm_matrix;
 
+typedef struct glm_peer glm_peer;       /* NVLink peer-memory Delta v exchange (4) */
+
 /* One subtask (the LocalSubproblem of solver.py:107-135) on device memory. */
 typedef struct {
     int32_t kind;
@@ -97,6 +99,7 @@ typedef struct {
                                L1; 2 stream the column L2 evict_first, view evict_last);
                                GLM_FLAG_REUSE_GSUM: base equals the previous solve's
                                base + delta (folded in place), reuse its g-sum for G(0) */
+    glm_peer *peer;         /* GLM_FLAG_PEER_FINALIZE: the round's Delta v exchange */
 } glm_solve_args;
 
 #define GLM_FLAG_REUSE_GSUM 4
@@ -104,6 +107,11 @@ typedef struct {
  * stream (from the advanced generator state) so it overlaps the caller's
  * fold / all-reduce; the next glm_solve of the same solver consumes it. */
 #define GLM_FLAG_PREFETCH_PERM 8
+/* Write B delta into this rank's peer-exchange buffer and publish it (with
+ * accumulate = 1: delta_out += delta; dv_out unused) — see glm_round_start. */
+#define GLM_FLAG_PEER_FINALIZE 32
+/* glm_round_start(mode 2) already started this solve (requires REUSE_GSUM). */
+#define GLM_FLAG_SKIP_BEGIN 64
 
 /* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */
 typedef struct {
@@ -332,6 +340,30 @@ int glm_stream_solve(glm_stream *s, const glm_stream_args *args, double *damping
 /* Per-chunk schedule of the last solve with GLM_STREAM_TIMING (PipelineSchedule,
  * pipeline.py:81-138): GLM_STREAM_SCHED_COLS doubles per chunk. */
 int glm_stream_schedule(const glm_stream *s, double *out, int capacity_rows, int *n_rows_out);
+
+/* ------------------------------ (4) fused Delta v exchange over peer memory
+ * The round's collective (allreduce_sum(v_bar) with canonical_sum's
+ * ascending-rank fold, engine.py:282, comm.py:41-46) fused with v += total
+ * (engine.py:306) and the next round's model + solve start (engine.py:
+ * 242-272, 148-166): one process per GPU, every rank's Delta v in its own HBM
+ * mapped into every peer through CUDA IPC (NVLink / NVSwitch).  A solve with
+ * GLM_FLAG_PEER_FINALIZE publishes its Delta v; glm_round_start waits for all
+ * ranks' publications (system-scope acquire), sums them in rank order (the
+ * same bits on every rank, = canonical_sum), applies them to v and runs the
+ * outer model; mode 2 also starts the solver (views, G(0), state).
+ * mode 0 only applies pending Delta v (before reading v). */
+int glm_peer_create(int device, int64_t n_rows, int rank, int world, glm_peer **out);
+size_t glm_peer_handle_bytes(void);
+int glm_peer_handle(const glm_peer *p, void *handle_out);
+/* handles: world x glm_peer_handle_bytes() bytes, rank order (all_gather) */
+int glm_peer_open(glm_peer *p, const void *handles);
+/* Mark any published, unapplied Delta v as consumed (engine reset). */
+int glm_peer_consume(glm_peer *p, void *stream);
+int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
+                    const double *target, double *v, int64_t n_rows, double *grad, double *lin,
+                    double *out_fv, double *cnst, double n_nodes, double n_devices, int epochs,
+                    double *scratch, void *stream);
+int glm_peer_destroy(glm_peer *p);
 
 #ifdef __cplusplus
 }

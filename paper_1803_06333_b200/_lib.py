@@ -19,6 +19,8 @@ CSC, DENSE = 0, 1
 MODE_SEQUENTIAL, MODE_ASYNC = 0, 1
 FLAG_REUSE_GSUM = 4
 FLAG_PREFETCH_PERM = 8
+FLAG_PEER_FINALIZE = 32
+FLAG_SKIP_BEGIN = 64
 STREAM_DELTA_IN, STREAM_VIEW_IN, STREAM_TIMING = 16, 32, 64
 STREAM_SCHED_COLS = 6
 
@@ -39,7 +41,7 @@ class GlmSolveArgs(ctypes.Structure):
                 ("quad", _c_dbl), ("cnst", _P), ("lin", _P), ("base", _P),
                 ("coord_target", _P), ("epochs", _c_i32), ("max_attempts", _c_i32),
                 ("group_lanes", _c_i32), ("max_inflight", _c_i32), ("reset_damping", _c_i32),
-                ("accumulate", _c_i32), ("flags", _c_i32)]
+                ("accumulate", _c_i32), ("flags", _c_i32), ("peer", _P)]
 
 
 class GlmSolveResult(ctypes.Structure):
@@ -115,6 +117,14 @@ SIGNATURES = {
     "glm_stream_info": (ctypes.c_int, [_P, _P]),
     "glm_stream_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "glm_stream_schedule": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
+    "glm_peer_create": (ctypes.c_int, [ctypes.c_int, _c_i64, ctypes.c_int, ctypes.c_int, _P]),
+    "glm_peer_handle_bytes": (ctypes.c_size_t, []),
+    "glm_peer_handle": (ctypes.c_int, [_P, _P]),
+    "glm_peer_open": (ctypes.c_int, [_P, _P]),
+    "glm_peer_consume": (ctypes.c_int, [_P, _P]),
+    "glm_round_start": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, _c_dbl, _P, _P, _c_i64,
+                                       _P, _P, _P, _P, _c_dbl, _c_dbl, ctypes.c_int, _P, _P]),
+    "glm_peer_destroy": (ctypes.c_int, [_P]),
 }
 
 _LIB = None

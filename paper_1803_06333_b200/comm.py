@@ -192,3 +192,54 @@ def make_reducer(kind="nccl", rank=None, peers=None, dim=None, deterministic=Fal
     if kind == "inproc":
         return InProcessReducer(1).participant(0)
     raise ValueError(f"unknown reducer {kind!r} (TCP reducers are replaced by NCCL)")
+
+
+class PeerExchange:
+    """The round's Delta v exchange over NVLink peer memory (csrc/peer.cu):
+    every rank's Delta v stays in its own HBM, mapped into every peer with
+    CUDA IPC; `glm_round_start` sums the ranks' buffers in ascending rank order
+    (the bits of canonical_sum on every rank, comm.py:41-46) fused with
+    v += total and the next round's model. World 1 works without IPC."""
+
+    def __init__(self, d, group=None, local=False):
+        import ctypes
+
+        from . import _lib as L
+        self.L = L
+        multi = dist.is_initialized() and not local
+        self.world = dist.get_world_size(group) if multi else 1
+        self.rank = dist.get_rank(group) if multi else 0
+        self.d = int(d)
+        h = ctypes.c_void_p()
+        L.check(L.lib().glm_peer_create(torch.cuda.current_device(), self.d, self.rank,
+                                        self.world, ctypes.byref(h)), "glm_peer_create")
+        self.handle = h
+        if self.world > 1:
+            nb = int(L.lib().glm_peer_handle_bytes())
+            mine = (ctypes.c_char * nb)()
+            L.check(L.lib().glm_peer_handle(h, mine), "glm_peer_handle")
+            got = [None] * self.world
+            dist.all_gather_object(got, bytes(mine), group=group)
+            blob = b"".join(got)
+            try:
+                L.check(L.lib().glm_peer_open(h, ctypes.c_char_p(blob)), "glm_peer_open")
+            except Exception:
+                L.lib().glm_peer_destroy(h)
+                self.handle = None
+                raise
+
+    def consume(self, stream):
+        from . import _device as D
+        self.L.check(self.L.lib().glm_peer_consume(self.handle, D.sptr(stream)),
+                     "glm_peer_consume")
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            self.L.lib().glm_peer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

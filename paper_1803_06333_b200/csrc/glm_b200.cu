@@ -6,3 +6,4 @@
 #include "data.cu"
 #include "api.cu"
 #include "stream.cu"
+#include "peer.cu"

@@ -1039,10 +1039,15 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         nbudget = narrow_budget(ep, sqm, a->max_inflight);
     }
     const int reuse = (a->flags & GLM_FLAG_REUSE_GSUM) ? 1 : 0;
-    count_launch();
-    begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1], a->lin,
-                                                            d, a->epochs, a->reset_damping,
-                                                            a->cnst, reuse);
+    // GLM_FLAG_SKIP_BEGIN: glm_round_start already reset the state, wrote the
+    // views and took G(0) from the cached g-sum (peer.cu)
+    const bool skip_begin = (a->flags & GLM_FLAG_SKIP_BEGIN) && reuse;
+    if (!skip_begin) {
+        count_launch();
+        begin_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1],
+                                                                a->lin, d, a->epochs,
+                                                                a->reset_damping, a->cnst, reuse);
+    }
     if (!reuse) {
         vp.mode = 0;
         count_launch();
@@ -1127,11 +1132,18 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         count_launch();
         empty_solve_kernel<<<1, 1, 0, stream>>>(s->st);
     }
-    count_launch();
-    finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
-        s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
-        delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0);
-    GLM_CUDA_TRY(cudaGetLastError());
+    if ((a->flags & GLM_FLAG_PEER_FINALIZE) && a->peer && a->accumulate && delta_out) {
+        // Delta v goes to this rank's peer-exchange buffer (peer.cu)
+        rc = peer_finalize(s, a->peer, a->lin, a->quad, m, d, delta_out,
+                           a->kind == GLM_DUAL_L2_SVM ? 1 : 0, stream);
+        if (rc) return rc;
+    } else {
+        count_launch();
+        finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
+            s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
+            delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
     s->last_epochs = a->epochs;
     s->last_m = m;
     if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0) {

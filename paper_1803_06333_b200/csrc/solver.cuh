@@ -44,6 +44,8 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
                 cudaStream_t stream);
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
 int join_prefetch(glm_solver *s, cudaStream_t stream);
+int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, int64_t m,
+                  int64_t d, double *alpha, int box, cudaStream_t stream);
 
 // ---- chunked (out-of-core) solves: stream.cu drives these per chunk.
 struct ChunkRecord {          // written by the close kernel into host-mapped memory

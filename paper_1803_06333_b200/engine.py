@@ -174,7 +174,7 @@ class Engine:
     def __init__(self, matrix, spec, config, reducer=None, cost_model=None, node_index=None,
                  measure_theta_bar=False, measure_theta_outer=False, chunk_runner=None,
                  mode=None, sync_solves=True, retry_budget=2, group_lanes=0, max_inflight=0,
-                 n_total=None, cache_flags=0):
+                 n_total=None, cache_flags=0, peer_exchange=True):
         if measure_theta_bar or measure_theta_outer:
             raise ValueError("theta measurement is the reference's CPU test-mode oracle "
                              "(solver.py:308-391); it is out of scope on the device path")
@@ -188,7 +188,10 @@ class Engine:
         self.stream = torch.cuda.current_stream()
         self.mode = {None: mode_for_threads(config.threads_per_device),
                      "sequential": L.MODE_SEQUENTIAL, "async": L.MODE_ASYNC}[mode]
-        self.sync_solves = sync_solves or self.mode == L.MODE_SEQUENTIAL
+        # sequential solves run the host retry loop unless the caller explicitly
+        # enqueues them (sync_solves=False: a fixed attempt budget per subtask)
+        self.sync_solves = sync_solves is not False and (sync_solves or
+                                                         self.mode == L.MODE_SEQUENTIAL)
         self.retry_budget = int(retry_budget)
         self.group_lanes = int(group_lanes)
         self.max_inflight = int(max_inflight)
@@ -254,6 +257,22 @@ class Engine:
         self.theta_bars = []
         self._theta_outer_last = None
         self.last_results = []
+        # Fused rounds (one local worker, t2 = 1, enqueued solves): the Delta v
+        # exchange runs over NVLink peer memory fused with the next round's start
+        # (csrc/peer.cu) instead of an NCCL all-reduce + 3 glue kernels; v then
+        # lags one round's Delta v until _flush_v() (before anything reads v).
+        self.exchange = None
+        self._pending = False
+        if (peer_exchange and len(self.workers) == 1 and config.t2 == 1
+                and chunk_runner is None and not self.sync_solves
+                and (self.reducer is None or getattr(self.reducer, "on_cuda", False))):
+            from .comm import PeerExchange
+            try:
+                self.exchange = PeerExchange(self.d, local=self.reducer is None)
+            except Exception:          # no P2P between the ranks' GPUs: NCCL path
+                self.exchange = None
+            if self.exchange is not None:
+                self.exchange.consume(self.stream)
 
     # -- state -----------------------------------------------------------------
     def _initial_v(self):
@@ -278,6 +297,9 @@ class Engine:
         fresh permutation streams and damping (no re-upload, no SpMV)."""
         self.alpha_dev.copy_(_D().to_device(self.spec.init_alpha()))
         self.v_dev.copy_(self._v0)
+        if self.exchange is not None:            # drop the last round's Delta v
+            self.exchange.consume(self.stream)
+            self._pending = False
         for (k, l), wk in self.workers.items():
             wk.gen.state = derive_seed(self.config.seed, k * self.config.devices + l)
             wk.solver.set_state(wk.gen.state, 1.0, self.stream)
@@ -319,12 +341,25 @@ class Engine:
         for wk in self.workers.values():
             wk.gsum_ok = False
 
+    def _flush_v(self):
+        """Apply the last fused round's Delta v to v (engine.py:306)."""
+        if self._pending:
+            L.check(L.lib().glm_round_start(
+                self.exchange.handle, None, 0, self.spec.index, self.spec.lam, None,
+                _D().ptr(self.v_dev), self.d, None, None, None, None, 1.0, 1.0, 0, None,
+                _D().sptr(self.stream)), "glm_round_start")
+            self._pending = False
+
     @property
     def v(self):
+        self._flush_v()
         return _D().to_host(self.v_dev[:self.d]).copy()
 
     @v.setter
     def v(self, value):
+        if self.exchange is not None:           # a pending Delta v no longer applies
+            self.exchange.consume(self.stream)
+            self._pending = False
         self.v_dev[:self.d] = _D().to_device(value)
 
     @property
@@ -392,9 +427,41 @@ class Engine:
                 self._solve_worker(wk, self.lin, cnst, first_inner=(t == 0), vbar=vbar)
         return vbar
 
+    def _outer_round_fused(self):
+        """One round with the exchange over peer memory: glm_round_start applies
+        the previous round's Delta v of every rank (canonical rank order), builds
+        the model and starts the solver; the solve publishes its Delta v."""
+        D = _D()
+        cfg = self.config
+        wk = next(iter(self.workers.values()))
+        reuse = wk.gsum_ok
+        L.check(L.lib().glm_round_start(
+            self.exchange.handle, wk.solver.handle, 2 if reuse else 1, self.spec.index,
+            self.spec.lam, D.ptr(self.row_target), D.ptr(self.v_dev), self.d, D.ptr(self.grad),
+            D.ptr(self.lin), D.ptr(self.scal[0:1]), D.ptr(self.scal[1:2]), float(cfg.nodes),
+            float(cfg.devices), int(cfg.epochs), D.ptr(D.scratch(self.stream)),
+            D.sptr(self.stream)), "glm_round_start")
+        self._pending = True
+        quad = cfg.sigma_bar_eff * cfg.sigma_eff * self.spec.beta
+        a_slice = self.alpha_dev[wk.lo:wk.hi]
+        flags = self.cache_flags | L.FLAG_PREFETCH_PERM | L.FLAG_PEER_FINALIZE | \
+            ((L.FLAG_REUSE_GSUM | L.FLAG_SKIP_BEGIN) if reuse else 0)
+        wk.last = wk.solver.solve(
+            wk.data, self.spec, lin=self.lin, cnst=self.scal[1:2], base=a_slice, quad=quad,
+            epochs=cfg.epochs, mode=self.mode, delta_out=a_slice, dv_out=None,
+            coord_target=wk.coord_target, reset_damping=True,
+            max_attempts=cfg.epochs + self.retry_budget, group_lanes=self.group_lanes,
+            max_inflight=self.max_inflight, accumulate=True, flags=flags, stream=self.stream,
+            peer=self.exchange)
+        wk.gsum_ok = True
+        self.last_results = []
+        self.stamp += 1
+
     def outer_round(self):
         """One outer round (engine.py:269-307): grad/f(v) fused with the first
         inner model, per-node t2 inner rounds, Delta v reduce, v += total."""
+        if self.exchange is not None:
+            return self._outer_round_fused()
         D = _D()
         cfg = self.config
         L.check(L.lib().glm_outer_model(
@@ -448,6 +515,7 @@ class Engine:
     def objective_and_gap(self):
         """(objective, gap) (engine.py:325-351) from the fused gap kernels."""
         self.check_solves()
+        self._flush_v()
         D = _D()
         a_local = self.alpha_dev[self.col_offset:self.col_offset + self.dm.n_cols]
         ct = None
@@ -506,6 +574,7 @@ class Engine:
                     reason = "time_budget"
                     break
         self.check_solves()
+        self._flush_v()
         alpha = self.alpha_global()
         self.spec.check_alpha(alpha)
         return TrainResult(model=Model(alpha, self.spec), trace=trace, v=self.v.copy(),

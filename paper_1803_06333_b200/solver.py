@@ -227,7 +227,7 @@ class DeviceSolver:
 
     def solve(self, dm, spec, *, lin, cnst, base, quad, epochs, mode, delta_out, dv_out,
               coord_target=None, reset_damping=False, max_attempts=0, group_lanes=0,
-              max_inflight=0, accumulate=False, flags=0, stream=None):
+              max_inflight=0, accumulate=False, flags=0, stream=None, peer=None):
         """Enqueue one subtask; if max_attempts == 0 returns the GlmSolveResult."""
         D = _D()
         a = L.GlmSolveArgs()
@@ -246,6 +246,7 @@ class DeviceSolver:
         a.max_inflight = int(max_inflight)
         a.accumulate = 1 if accumulate else 0
         a.flags = int(flags)
+        a.peer = peer.handle if peer is not None else None
         a.reset_damping = 1 if reset_damping else 0
         res = L.GlmSolveResult()
         st = L.lib().glm_solve(self.handle, ctypes.byref(dm.struct), ctypes.byref(a),

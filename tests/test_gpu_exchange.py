@@ -1,0 +1,91 @@
+"""The fused Delta v exchange + round start (csrc/peer.cu) against the
+unfused engine round (solve -> all-reduce -> v += total -> outer model ->
+begin): identical bits in deterministic mode, on one GPU and — when the box
+has two — across two processes over NVLink peer memory vs the deterministic
+NCCL reducer (all-gather + ascending-rank fold = canonical_sum)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_1803_06333_b200 as g  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _synth(n, d, k, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.integers(0, d - k + 1, size=(n, k)), axis=1) + np.arange(k)
+    vals = rng.standard_normal((n, k))
+    vals /= np.linalg.norm(vals, axis=1, keepdims=True)
+    vals *= np.where(rng.standard_normal(n) >= 0, 1.0, -1.0)[:, None]
+    indptr = np.arange(0, n * k + 1, k, dtype=np.int64)
+    return g.SparseColumnMatrix(d, indptr, rows.reshape(-1).astype(np.int32), vals.reshape(-1))
+
+
+@pytest.mark.parametrize("kind", ["dual_l2_logistic", "dual_l2_svm", "ridge_primal"])
+def test_fused_round_bit_identical_single_gpu(kind):
+    m = _synth(6_000, 900, 8, 3)
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    if kind == "ridge_primal":
+        tgt = np.random.default_rng(1).standard_normal(m.n_rows)
+        spec = g.ObjectiveSpec(kind, 1.0, m.n_rows, m.n_cols, target=tgt)
+        k = 2
+    else:
+        tgt = None
+        spec = g.ObjectiveSpec(kind, 1.0, m.n_cols, m.n_rows)
+        k = 0 if kind == "dual_l2_logistic" else 1
+    cfg = g.HierarchyConfig(t1=6, seed=5, epochs=2)
+    runs = []
+    for peer in (False, True):
+        eng = g.Engine(m, spec, cfg, mode="sequential", sync_solves=False, retry_budget=4,
+                       peer_exchange=peer)
+        assert (eng.exchange is not None) == peer
+        runs.append(eng.train(g.StoppingCriteria(max_rounds=6)))
+    np.testing.assert_array_equal(runs[0].trace.objectives(), runs[1].trace.objectives())
+    np.testing.assert_array_equal(runs[0].model.alpha, runs[1].model.alpha)
+    np.testing.assert_array_equal(runs[0].v, runs[1].v)
+    want = oracle.train(om, k, 1.0, target=tgt, epochs=2, seed=5, rounds=6)
+    np.testing.assert_allclose(runs[1].trace.objectives(), want["objective"], rtol=1e-10)
+
+
+def test_fused_round_reset_and_graph_replay():
+    """reset() drops the pending Delta v; a captured graph of fused rounds
+    replays to the same trajectory as eager rounds."""
+    m = _synth(20_000, 2_000, 10, 8)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
+    eng = g.Engine(m, spec, g.HierarchyConfig(seed=2, epochs=1), mode="sequential",
+                   sync_solves=False)
+    for _ in range(4):
+        eng.outer_round()
+    v_eager, a_eager = eng.v, eng.alpha
+    eng.reset()
+    graph = eng.capture(4)
+    eng.reset()
+    graph.replay()
+    torch.cuda.synchronize()
+    eng._pending = True                     # the replayed rounds left their Delta v pending
+    np.testing.assert_array_equal(eng.alpha, a_eager)
+    np.testing.assert_array_equal(eng.v, v_eager)
+
+
+def test_two_process_exchange_matches_nccl():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", "29533",
+         os.path.join(ROOT, "tests", "mp_exchange_check.py")],
+        capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
