@@ -286,7 +286,7 @@ def ours_main(args):
         return g.Engine(dm, spec, cfg, reducer=reducer, node_index=rank if world > 1 else None,
                         mode="async", sync_solves=False, retry_budget=0,
                         n_total=N_EX if world > 1 else None, group_lanes=args.lanes,
-                        cache_flags=args.cache_flags)
+                        cache_flags=args.cache_flags, peer_exchange=bool(args.peer))
 
     eng = make_engine()
     phase("engine ready", rank)
@@ -395,8 +395,6 @@ def ours_main(args):
     # microbenchmark doing exactly the epoch's nnz_loc gathers + reds into a
     # d-double vector (tools/l2_random_roofline.cu); frac > ~0.9 means the
     # epoch kernel runs at the L2 random-access limit, not an HBM one.
-    if rank == 0:
-        roofline["l2_random_ceiling"] = l2_ceiling(nnz_loc, epoch_ms)
 
     phase("timed region done", rank)
     # -------- e2e through the reference-facing C-ABI with host buffers
@@ -427,6 +425,7 @@ def ours_main(args):
         cpu = cpu_arm(args, budget_s=args.cpu_budget)
 
     if rank == 0:
+        roofline["l2_random_ceiling"] = l2_ceiling(nnz_loc, epoch_ms)
         clocks = clk.summary()
         line = {"metric": METRIC, "value": value, "unit": "epochs/s", "n_gpus": world,
                 "steps": steps_timed, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -478,20 +477,35 @@ def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world
     for _ in range(2):
         out = device_solve_host(h, sub, gen_state, damping, 1, 1, out=(dl, dvb))
     torch.cuda.synchronize()
+    if world > 1:                    # every rank enters the timed loop together
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+    t_solve = []
+    t_red = []
     t0 = time.perf_counter()
     for _ in range(steps):
+        ta = time.perf_counter()
         out = device_solve_host(h, sub, gen_state, damping, 1, 1, out=(dl, dvb))
         _lib.check(int(out[7]), "glm_device_solve")
+        tb = time.perf_counter()
         if reducer is not None:
             reducer.allreduce_sum(dvb)
+        t_solve.append(tb - ta)
+        t_red.append(time.perf_counter() - tb)
     el = time.perf_counter() - t0
+    phase(f"e2e loop {el:.4f}s, solves {sum(t_solve):.4f}s, reduces {sum(t_red):.4f}s",
+          int(os.environ.get("RANK", "0")))
     el = max_over_ranks(el, world)
     _lib.lib().glm_ctx_destroy(h)
     return {"value": steps / el, "unit": "epochs/s",
             "h2d_bytes_per_step": 8 * (d + m + 1), "d2h_bytes_per_step": 8 * (m + d),
             "path": "glm_device_solve (host buffers, pinned) per rank"
                     + (" + host Delta-v allreduce" if reducer is not None else ""),
-            "timer": "host wall clock around the plugin call (includes copies)"}
+            "timer": "host wall clock around the plugin call (includes copies)",
+            "median_solve_ms": 1e3 * float(np.median(t_solve)),
+            "max_solve_ms": 1e3 * float(np.max(t_solve)),
+            "median_host_allreduce_ms": 1e3 * float(np.median(t_red)),
+            "max_host_allreduce_ms": 1e3 * float(np.max(t_red))}
 
 
 def main():
@@ -515,6 +529,9 @@ def main():
     ap.add_argument("--lanes", type=int, default=0,
                     help="lanes per coordinate | registers << 8 (0 = auto; tools/sweep_c2.py)")
     ap.add_argument("--cache-flags", type=int, default=1, help="glm_solve_args.flags")
+    ap.add_argument("--peer", type=int, default=1,
+                    help="Delta-v exchange over NVLink peer memory fused with the round "
+                         "start (0: NCCL all-reduce + separate glue kernels)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

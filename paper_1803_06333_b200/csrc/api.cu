@@ -130,6 +130,7 @@ int glm_solver_destroy(glm_solver *s) {
     cudaFree(s->view[0]);
     cudaFree(s->view[1]);
     cudaFree(s->perm);
+    cudaFree(s->perm_b);
     cudaFree(s->perm_mem);
     cudaFree(s->partials);
     cudaFree(s->gpart);
@@ -170,6 +171,7 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     chk(cudaMalloc(&s->view[0], sizeof(double) * mr));
     chk(cudaMalloc(&s->view[1], sizeof(double) * mr));
     chk(cudaMalloc(&s->perm, sizeof(int32_t) * mc));
+    chk(cudaMalloc(&s->perm_b, sizeof(int32_t) * mc));
     size_t pb = perm_scratch_bytes((int64_t)mc);
     chk(cudaMalloc(&s->perm_mem, pb));
     chk(cudaMalloc(&s->partials, sizeof(double) * 3 * 8 * NUM_SMS));

@@ -76,11 +76,12 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
         const uint64_t g = warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
         if (threadIdx.x == 0) st->gen_next = g;
     }
-    __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {     // the block's writes (observed through the barrier)
+        __threadfence_system(); // before its arrival; the last block then releases
         s_last = atomicAdd(reinterpret_cast<unsigned long long *>(ctl + 2), 1ull) ==
                  (unsigned long long)(gridDim.x - 1);
+    }
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
         ctl[2] = 0;

@@ -930,6 +930,8 @@ int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t st
     int rc = join_prefetch(s, stream);
     if (rc) return rc;
     s->prefetched = false;               // the stream state changes
+    s->host_known = true;
+    s->host_gen = gen_state ? gen_state : 0x9E3779B97F4A7C15ULL;
     count_launch();
     set_state_kernel<<<1, 1, 0, stream>>>(s->st, gen_state ? gen_state : 0x9E3779B97F4A7C15ULL,
                                           damping);
@@ -1063,8 +1065,28 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     if (s->prefetched) {
         GLM_CUDA_TRY(cudaStreamWaitEvent(stream, s->ev_join, 0));
         have_perm0 = s->prefetch_m == m;
+        if (have_perm0 && s->prefetch_alt) s->perm_cur ^= 1;
         s->prefetched = false;
     }
+    int32_t *P = s->perm_cur ? s->perm_b : s->perm;
+    int32_t *P_alt = s->perm_cur ? s->perm : s->perm_b;
+    ep.perm = P;
+    // Early prefetch: with one attempt per solve the generator advances by
+    // exactly m keys, so the host knows the next solve's start state and its
+    // permutation can be generated on the side stream into the other buffer
+    // while this solve's epoch runs (overlapping value / finalize / the round
+    // start instead of sitting between them and the next epoch).
+    const bool early = (a->flags & GLM_FLAG_PREFETCH_PERM) && s->host_known &&
+                       a->max_attempts == 1 && a->epochs == 1 && m > 0;
+    const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
+    auto ensure_side = [&]() -> int {
+        if (!s->side) {
+            GLM_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        }
+        return GLM_OK;
+    };
     int launched = 0;
     auto attempt = [&]() -> int {
         // optional CUDA-event bracket: [perm | snapshot+epoch | value]
@@ -1080,8 +1102,18 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         }
         int r = GLM_OK;
         if (!(launched == 0 && have_perm0))
-            r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, s->perm, ps, stream);
+            r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, P, ps, stream);
         if (r) return r;
+        if (early && launched == 0) {
+            if ((r = ensure_side())) return r;
+            GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+            GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+            if ((r = stream_perm(nullptr, next_state, 0, m, P_alt, ps, s->side))) return r;
+            GLM_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
+            s->prefetched = true;
+            s->prefetch_m = m;
+            s->prefetch_alt = true;
+        }
         if (s->timing) GLM_CUDA_TRY(event_record(ev[1], stream));
         if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
             count_launch();
@@ -1146,21 +1178,23 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     }
     s->last_epochs = a->epochs;
     s->last_m = m;
-    if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0) {
-        // generate the next solve's attempt-0 permutation from gen_next while the
-        // caller runs its fold / all-reduce / round-start kernels
-        if (!s->side) {
-            GLM_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
-            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
-            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    if (early) {
+        s->host_gen = next_state;
+    } else {
+        s->host_known = false;
+        if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0) {
+            // generate the next solve's attempt-0 permutation from gen_next while
+            // the caller runs its fold / all-reduce / round-start kernels
+            if ((rc = ensure_side())) return rc;
+            GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+            GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+            rc = stream_perm_from(&s->st->gen_next, m, P, ps, s->side);
+            if (rc) return rc;
+            GLM_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
+            s->prefetched = true;
+            s->prefetch_m = m;
+            s->prefetch_alt = false;
         }
-        GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
-        GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
-        rc = stream_perm_from(&s->st->gen_next, m, s->perm, ps, s->side);
-        if (rc) return rc;
-        GLM_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
-        s->prefetched = true;
-        s->prefetch_m = m;
     }
     if (res) return read_result(s, res, nullptr, 0, stream);
     return GLM_OK;

@@ -23,8 +23,13 @@ struct glm_solver {
     int timing = 0;                       // record per-attempt CUDA events
     cudaStream_t side = nullptr;          // permutation prefetch stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool prefetched = false;              // perm holds the next solve's attempt 0
+    bool prefetched = false;              // a buffer holds the next solve's attempt 0
     int64_t prefetch_m = 0;
+    bool prefetch_alt = false;            // ... in the other buffer (early prefetch)
+    int32_t *perm_b = nullptr;            // second permutation buffer
+    int perm_cur = 0;                     // 0: perm, 1: perm_b
+    bool host_known = false;              // host_gen == the device's next start state
+    uint64_t host_gen = 0;
     std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
     int last_epochs = 0;
     int64_t last_m = 0;
