@@ -191,7 +191,9 @@ int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, i
                   int64_t d, double *alpha, int box, cudaStream_t stream) {
     if (pr->d != d) return glm_set_error(GLM_USAGE, "peer exchange sized for another d");
     count_launch();
-    peer_finalize_kernel<<<PEER_BLOCKS, PEER_THREADS, 0, stream>>>(
+    int64_t blocks = ((m > d ? m : d) + 4 * PEER_THREADS - 1) / (4 * PEER_THREADS);
+    blocks = blocks < 1 ? 1 : (blocks > 8 * NUM_SMS ? 8 * NUM_SMS : blocks);
+    peer_finalize_kernel<<<(int)blocks, PEER_THREADS, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], lin, quad, m, d, alpha, box,
         pr->dv, pr->ctl);
     GLM_CUDA_TRY(cudaGetLastError());

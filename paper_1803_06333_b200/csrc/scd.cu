@@ -55,6 +55,7 @@ struct EpochParams {
     double *gpart;          // per-block partial sum_j g(base_j + delta_j) of the epoch
     int64_t nnz;
     int64_t seq;            // chunked mode: run only while chunk `seq` is open (-1: always)
+    int reserve_blocks;     // async: block slots left free for the side-stream permutation
 };
 
 // A kernel of chunk `seq` runs only while that chunk is open and unfinished;
@@ -750,7 +751,8 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     if (groups > p.m) groups = p.m;
     if (groups < 32 / G) groups = 32 / G;
     const int64_t need_blocks = (groups * G + 255) / 256;
-    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
+    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS - p.reserve_blocks;
+    if (cap < NUM_SMS) cap = NUM_SMS;
     if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
     const int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
     count_launch();
@@ -1026,6 +1028,14 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     const double avg = dense ? (double)d : (m > 0 ? (double)A->nnz / (double)m : 0.0);
     const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg);
     const int seq_bs = avg <= 96.0 ? 32 : 256;
+    // the per-attempt value pass over the view: ~4 rows per thread keeps the
+    // block partials (and the last block's fold) short
+    auto value_grid_view = [](int64_t n) {
+        int64_t b = (n + 4 * VALUE_THREADS - 1) / (4 * VALUE_THREADS);
+        if (b < 1) b = 1;
+        if (b > 2 * NUM_SMS) b = 2 * NUM_SMS;
+        return (int)b;
+    };
     auto value_grid = [](int64_t n) {
         int64_t b = (n + VALUE_THREADS - 1) / VALUE_THREADS;
         if (b < 1) b = 1;
@@ -1071,6 +1081,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     int32_t *P = s->perm_cur ? s->perm_b : s->perm;
     int32_t *P_alt = s->perm_cur ? s->perm : s->perm_b;
     ep.perm = P;
+    ep.reserve_blocks = 0;
     // Early prefetch: with one attempt per solve the generator advances by
     // exactly m keys, so the host knows the next solve's start state and its
     // permutation can be generated on the side stream into the other buffer
@@ -1132,7 +1143,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         if (r) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[2], stream));
         count_launch();
-        value_kernel<<<value_grid(d), VALUE_THREADS, 0, stream>>>(vp);
+        value_kernel<<<value_grid_view(d), VALUE_THREADS, 0, stream>>>(vp);
         GLM_CUDA_TRY(cudaGetLastError());
         if (s->timing) {
             GLM_CUDA_TRY(event_record(ev[3], stream));
