@@ -40,7 +40,7 @@ def test_train_predict_eval_match_reference(golden, tmp_path, capsys):
     data = _tiny_svm(golden, tmp_path / "tiny.svm")
     z = golden("predict")
     cfg = tmp_path / "run.cfg"
-    cfg.write_text("# config file: flags win\nlambda = 0.5\nepochs = 2\nseed = 99\n")
+    cfg.write_text("# config file (keys are flag dests; flags win)\nlam = 0.5\nepochs = 2\nseed = 99\n")
     model, trace = tmp_path / "m.bin", tmp_path / "trace.csv"
     rc = cli.main(["--config", str(cfg), "train", "--data", str(data), "--objective",
                    "dual-logistic", "--max-rounds", "5", "--seed", "3", "--model-out",
