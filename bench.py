@@ -286,7 +286,8 @@ def ours_main(args):
         return g.Engine(dm, spec, cfg, reducer=reducer, node_index=rank if world > 1 else None,
                         mode="async", sync_solves=False, retry_budget=0,
                         n_total=N_EX if world > 1 else None, group_lanes=args.lanes,
-                        cache_flags=args.cache_flags, peer_exchange=bool(args.peer))
+                        cache_flags=args.cache_flags, peer_exchange=bool(args.peer),
+                        max_inflight=args.inflight)
 
     eng = make_engine()
     phase("engine ready", rank)
@@ -529,6 +530,8 @@ def main():
     ap.add_argument("--lanes", type=int, default=0,
                     help="lanes per coordinate | registers << 8 (0 = auto; tools/sweep_c2.py)")
     ap.add_argument("--cache-flags", type=int, default=1, help="glm_solve_args.flags")
+    ap.add_argument("--inflight", type=int, default=0,
+                    help="async coordinates in flight (0 = the feature-conflict budget)")
     ap.add_argument("--peer", type=int, default=1,
                     help="Delta-v exchange over NVLink peer memory fused with the round "
                          "start (0: NCCL all-reduce + separate glue kernels)")
