@@ -104,6 +104,9 @@ struct glm_stream {
     std::deque<glm::LoadJob> jobs;     // posted, in order
     std::vector<glm::LoadJob> finished;
     bool quit = false;
+    int64_t next_key = 0;              // unique load-job keys across solves
+    struct Carry { int chunk, slot; int64_t key; };
+    std::vector<Carry> carried;        // loads posted for the next solve's first streamed chunks
     int load_error = 0;
     std::string load_msg;
     // schedule of the last solve: rows of GLM_STREAM_SCHED_COLS doubles
@@ -512,12 +515,15 @@ int glm_stream_solve(glm_stream *S, const glm_stream_args *a, double *damping_io
     const int64_t m = S->m, d = S->d;
     const int C = S->n_chunks;
     cudaStream_t cs = S->cs;
-    struct Drain {   // on every exit: let the loader finish, forget its results
+    struct Drain {   // failed solve: let the loader finish, forget its results
         glm_stream *S;
+        bool ok = false;
         ~Drain() {
+            if (ok) return;   // loads carried into the next solve keep running
             std::unique_lock<std::mutex> lk(S->mu);
             S->cv.wait(lk, [&] { return S->jobs.empty() || S->quit; });
             S->finished.clear();
+            S->carried.clear();
             lk.unlock();
             cudaStreamSynchronize(S->xs);
             cudaStreamSynchronize(S->cs);
@@ -570,6 +576,38 @@ int glm_stream_solve(glm_stream *S, const glm_stream_args *a, double *damping_io
         if ((int)(q % C) >= S->n_res) streamed.push_back(q);
     size_t next_post = 0;
     int free_slots[2] = {1, 1};
+    std::vector<int64_t> key_of(jobs.size(), -1);
+    auto wait_key = [&](int64_t key, double *ms) -> int {
+        std::unique_lock<std::mutex> lk(S->mu);
+        for (;;) {
+            if (S->load_error) return glm_set_error(S->load_error, S->load_msg.c_str());
+            for (size_t i = 0; i < S->finished.size(); ++i)
+                if (S->finished[i].seq == key) {
+                    if (ms) *ms = S->finished[i].load_ms;
+                    S->finished.erase(S->finished.begin() + i);
+                    return GLM_OK;
+                }
+            S->cv.wait(lk);
+        }
+    };
+    {   // loads the previous solve posted ahead become this solve's first streamed chunks
+        std::vector<glm_stream::Carry> carried;
+        {
+            std::lock_guard<std::mutex> lk(S->mu);
+            carried.swap(S->carried);
+        }
+        for (const auto &cj : carried) {
+            if (next_post < streamed.size() && (int)(streamed[next_post] % C) == cj.chunk) {
+                const int64_t q = streamed[next_post++];
+                slot_of[q] = cj.slot;
+                key_of[q] = cj.key;
+                free_slots[cj.slot] = 0;
+            } else {
+                int r = wait_key(cj.key, nullptr);   // a stale carry: let it land first
+                if (r) return r;
+            }
+        }
+    }
     auto post_loads = [&]() {
         std::lock_guard<std::mutex> lk(S->mu);
         while (next_post < streamed.size()) {
@@ -578,27 +616,16 @@ int glm_stream_solve(glm_stream *S, const glm_stream_args *a, double *damping_io
             free_slots[sl] = 0;
             const int64_t q = streamed[next_post++];
             slot_of[q] = sl;
+            key_of[q] = S->next_key++;
             LoadJob j;
-            j.seq = q;
+            j.seq = key_of[q];
             j.chunk = (int)(q % C);
             j.slot = sl;
             S->jobs.push_back(j);
         }
         S->cv.notify_all();
     };
-    auto wait_loaded = [&](int64_t q) -> int {
-        std::unique_lock<std::mutex> lk(S->mu);
-        for (;;) {
-            if (S->load_error) return glm_set_error(S->load_error, S->load_msg.c_str());
-            for (size_t i = 0; i < S->finished.size(); ++i)
-                if (S->finished[i].seq == q) {
-                    load_ms[q] = S->finished[i].load_ms;
-                    S->finished.erase(S->finished.begin() + i);
-                    return GLM_OK;
-                }
-            S->cv.wait(lk);
-        }
-    };
+    auto wait_loaded = [&](int64_t q) -> int { return wait_key(key_of[q], &load_ms[q]); };
     const double t_solve0 = now_ms();
     double h2d_wait_ms = 0.0;
     auto enqueue = [&](int64_t q, bool fresh) -> int {
@@ -751,6 +778,24 @@ int glm_stream_solve(glm_stream *S, const glm_stream_args *a, double *damping_io
         scal_out[2] = now_ms() - t_solve0;
         scal_out[3] = h2d_wait_ms;
     }
+    if (S->n_res < C) {
+        // The next solve (the next outer round) starts with the same streamed
+        // chunks: load them now, while the caller folds, exchanges and rebuilds
+        // its model, so the next solve's first chunks need no wait.
+        std::lock_guard<std::mutex> lk(S->mu);
+        const int first = S->n_res, second = S->n_res + 1 < C ? S->n_res + 1 : S->n_res;
+        const int ch[2] = {first, second};
+        for (int i = 0; i < 2; ++i) {
+            LoadJob j;
+            j.seq = S->next_key++;
+            j.chunk = ch[i];
+            j.slot = i;
+            S->jobs.push_back(j);
+            S->carried.push_back({ch[i], i, j.seq});
+        }
+        S->cv.notify_all();
+    }
+    drain.ok = true;
     return GLM_OK;
 }
 
