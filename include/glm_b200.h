@@ -365,6 +365,22 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
                     double *scratch, void *stream);
 int glm_peer_destroy(glm_peer *p);
 
+/* --------------------------------------- (5) host ingest: svmlight parser
+ * parse_svmlight (data.py:190-239), multi-threaded: `<label> <idx>:<val> ...`
+ * lines, 1-based strictly increasing indices, blank / '#' lines skipped.
+ * info[7] = n_examples, nnz, max feature index, error kind (0 ok, 1 bad label,
+ * 2 bad feature token, 3 index < 1, 4 not increasing, 5 index out of int32
+ * range), error line (1-based), token offset, token length.  On success
+ * *out holds the result until glm_svmlight_free; glm_svmlight_fetch fills the
+ * example-major CSC (indptr i64[n+1], rows i32[nnz], vals f64[nnz]) and the
+ * labels f64[n]. */
+typedef struct glm_svmlight glm_svmlight;
+int glm_svmlight_parse(const char *text, int64_t len, int n_threads, glm_svmlight **out,
+                       int64_t *info);
+int glm_svmlight_fetch(const glm_svmlight *r, int64_t *indptr, int32_t *rows, double *vals,
+                       double *labels);
+int glm_svmlight_free(glm_svmlight *r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,3 +7,4 @@
 #include "api.cu"
 #include "stream.cu"
 #include "peer.cu"
+#include "ingest.cu"

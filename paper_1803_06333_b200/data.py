@@ -14,6 +14,7 @@ partition of columns is a zero-copy view (indptr offset, shared rows/vals).
 from __future__ import annotations
 
 import ctypes
+import io
 import struct
 from dataclasses import dataclass, field
 
@@ -382,15 +383,65 @@ def hstack(blocks):
 
 
 # --------------------------------------------------------------- svmlight
-def parse_svmlight(stream):
+# Characters whose meaning differs between Python's line/field splitting and
+# the native parser's ASCII grammar: inputs containing them take the
+# line-by-line path below, which follows data.py:190-239 exactly.
+_NATIVE_UNSAFE = ("\x0b", "\x0c", "\x1c", "\x1d", "\x1e", "\x1f")
+
+
+def parse_svmlight(stream, n_threads=0):
     """svmlight text -> (example-major matrix, labels) (data.py:190-239).
 
-    Host ingest (SURVEY §8(f) next #1); same validation and messages."""
+    Host ingest: text from a str or a file object is parsed
+    by the multi-threaded native parser (csrc/ingest.cu, `glm_svmlight_parse`);
+    exotic input (non-ASCII, or separators Python splits on but the native
+    grammar does not) and every error case run the line-by-line path, so the
+    values, the arrays and the error messages are those of the reference."""
     if isinstance(stream, str):
-        stream = stream.splitlines()
+        text, str_input = stream, True
+    elif hasattr(stream, "read"):
+        text, str_input = stream.read(), False
+        if isinstance(text, bytes):
+            text = text.decode()
+    else:
+        return _parse_svmlight_lines(stream)
+    res = _parse_svmlight_native(text, str_input, n_threads)
+    if res is not None:
+        return res
+    return _parse_svmlight_lines(text.splitlines() if str_input else io.StringIO(text))
+
+
+def _parse_svmlight_native(text, str_input, n_threads):
+    if not text.isascii() or any(c in text for c in _NATIVE_UNSAFE) or \
+            (str_input and "\r" in text):
+        return None
+    data = text.encode()
+    lib = L.lib()
+    h = ctypes.c_void_p()
+    info = np.zeros(7, dtype=np.int64)
+    L.check(lib.glm_svmlight_parse(data, len(data), int(n_threads), ctypes.byref(h),
+                                   info.ctypes.data_as(ctypes.c_void_p)), "glm_svmlight_parse")
+    if info[3] != 0:
+        return None                      # the line path raises the reference's error
+    n, nnz, max_feat = int(info[0]), int(info[1]), int(info[2])
+    indptr = np.empty(n + 1, dtype=np.int64)
+    rows = np.empty(nnz, dtype=np.int32)
+    vals = np.empty(nnz, dtype=np.float64)
+    labels = np.empty(n, dtype=np.float64)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    try:
+        L.check(lib.glm_svmlight_fetch(h, vp(indptr), vp(rows), vp(vals), vp(labels)),
+                "glm_svmlight_fetch")
+    finally:
+        lib.glm_svmlight_free(h)
+    return SparseColumnMatrix(max_feat, indptr, rows, vals), labels
+
+
+def _parse_svmlight_lines(lines):
+    """The reference's line loop (data.py:198-239), same validation/messages."""
     labels, indptr, rows, vals = [], [0], [], []
     max_feat = 0
-    for lineno, line in enumerate(stream, start=1):
+    for lineno, line in enumerate(lines, start=1):
         line = line.strip()
         if not line or line.startswith("#"):
             continue
