@@ -345,6 +345,8 @@ def ours_main(args):
 
     phase("warm-up + capture done", rank)
     kern_ms = np.zeros(3)
+    glue_ms = np.zeros(3)
+    glue_n = np.zeros(3)
     attempts = 0
     with ClockSampler(local) as clk:
         t_w = time.perf_counter()          # keep the GPU busy while nvidia-smi starts
@@ -361,6 +363,9 @@ def ours_main(args):
                 k_ms, k_n = wk.solver.timing_read(consume=False)
                 kern_ms += k_ms
                 attempts += k_n
+                g_ms, g_n = wk.solver.timing_glue(consume=False)
+                glue_ms += g_ms
+                glue_n += g_n
         launches = lib.glm_launch_count() - launches0
         if graph is None:
             k_ms, attempts = wk.solver.timing_read()
@@ -390,6 +395,9 @@ def ours_main(args):
                 "step_breakdown_ms": {"permutation": kern_ms[0] / max(attempts, 1),
                                       "epoch": epoch_ms,
                                       "value_damping": kern_ms[2] / max(attempts, 1),
+                                      "finalize_publish": glue_ms[0] / max(glue_n[0], 1),
+                                      "round_start": glue_ms[1] / max(glue_n[1], 1),
+                                      "round_turn": glue_ms[2] / max(glue_n[2], 1),
                                       "step": ms_step}}
     # The epoch's real ceiling: every nnz is one random 8-byte gather and one
     # random f64 red into the L2-resident shared vector.  Measured live by a

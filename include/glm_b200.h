@@ -112,6 +112,9 @@ typedef struct {
 #define GLM_FLAG_PEER_FINALIZE 32
 /* glm_round_start(mode 2) already started this solve (requires REUSE_GSUM). */
 #define GLM_FLAG_SKIP_BEGIN 64
+/* One attempt (epochs = max_attempts = 1) whose value check, finalize and
+ * Delta v exchange are left to glm_round_turn on the same stream. */
+#define GLM_FLAG_TURN 128
 
 /* Result of a subtask (SubtaskResult, solver.py:138-149 + DampingState). */
 typedef struct {
@@ -189,6 +192,10 @@ int glm_solver_timing_read(glm_solver *s, double *ms_out, int32_t *n_out);
 /* Same sums without releasing the events (graph-captured attempts re-record
  * them on every replay). */
 int glm_solver_timing_peek(glm_solver *s, double *ms_out, int32_t *n_out);
+/* Finalize ([0]), glm_round_start ([1]) and glm_round_turn ([2]) kernels
+ * bracketed while timing is on: ms_out[3] sums, n_out[3] counts; consume = 0
+ * keeps graph-captured events. */
+int glm_solver_timing_glue(glm_solver *s, double *ms_out, int32_t *n_out, int consume);
 /* Make `stream` wait for a pending permutation prefetch (before ending a
  * graph capture or reusing the solver from another stream). */
 int glm_solver_join(glm_solver *s, void *stream);
@@ -364,6 +371,14 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
                     double *out_fv, double *cnst, double n_nodes, double n_devices, int epochs,
                     double *scratch, void *stream);
 int glm_peer_destroy(glm_peer *p);
+/* After a GLM_FLAG_TURN solve: the attempt's value check and damping decision,
+ * alpha += delta, publish Delta v, wait for every rank's, v += their rank-order
+ * sum, and the next round's model and solver start — one kernel (peer.cu).
+ * cnst holds this round's const on entry and the next round's on exit. */
+int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad,
+                   double *cnst, double *alpha, int64_t m, const double *target, double *v,
+                   int64_t n_rows, double *grad, double *lin, double *out_fv, double n_nodes,
+                   double n_devices, int epochs, double *scratch, void *stream);
 
 /* --------------------------------------- (5) host ingest: svmlight parser
  * parse_svmlight (data.py:190-239), multi-threaded: `<label> <idx>:<val> ...`

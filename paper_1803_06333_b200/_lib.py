@@ -21,6 +21,7 @@ FLAG_REUSE_GSUM = 4
 FLAG_PREFETCH_PERM = 8
 FLAG_PEER_FINALIZE = 32
 FLAG_SKIP_BEGIN = 64
+FLAG_TURN = 128
 STREAM_DELTA_IN, STREAM_VIEW_IN, STREAM_TIMING = 16, 32, 64
 STREAM_SCHED_COLS = 6
 
@@ -67,6 +68,7 @@ SIGNATURES = {
     "glm_solver_timing": (ctypes.c_int, [_P, ctypes.c_int]),
     "glm_solver_timing_read": (ctypes.c_int, [_P, _P, _P]),
     "glm_solver_timing_peek": (ctypes.c_int, [_P, _P, _P]),
+    "glm_solver_timing_glue": (ctypes.c_int, [_P, _P, _P, ctypes.c_int]),
     "glm_device_count": (ctypes.c_int, [_P]),
     "glm_xorshift_jump": (_c_u64, [_c_u64, _c_u64]),
     "glm_derive_seed": (_c_u64, [_c_u64, _P, ctypes.c_int]),
@@ -125,6 +127,9 @@ SIGNATURES = {
     "glm_round_start": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, _c_dbl, _P, _P, _c_i64,
                                        _P, _P, _P, _P, _c_dbl, _c_dbl, ctypes.c_int, _P, _P]),
     "glm_peer_destroy": (ctypes.c_int, [_P]),
+    "glm_round_turn": (ctypes.c_int, [_P, _P, ctypes.c_int, _c_dbl, _c_dbl, _P, _P, _c_i64, _P,
+                                      _P, _c_i64, _P, _P, _P, _c_dbl, _c_dbl, ctypes.c_int, _P,
+                                      _P]),
     "glm_svmlight_parse": (ctypes.c_int, [_P, _c_i64, ctypes.c_int, _P, _P]),
     "glm_svmlight_fetch": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "glm_svmlight_free": (ctypes.c_int, [_P]),

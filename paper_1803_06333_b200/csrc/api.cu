@@ -97,6 +97,26 @@ int glm_solver_timing_peek(glm_solver *s, double *ms_out, int32_t *n_out) {
     return timing_sum(s, ms_out, n_out, false);
 }
 
+int glm_solver_timing_glue(glm_solver *s, double *ms_out, int32_t *n_out, int consume) {
+    if (!s) return glm_set_error(GLM_USAGE, "null solver");
+    double acc[3] = {0.0, 0.0, 0.0};
+    int32_t n[3] = {0, 0, 0};
+    for (auto &g : s->glue_events) {
+        GLM_CUDA_TRY(cudaEventSynchronize(g.second[1]));
+        float t = 0.f;
+        GLM_CUDA_TRY(cudaEventElapsedTime(&t, g.second[0], g.second[1]));
+        acc[g.first] += t;
+        n[g.first] += 1;
+    }
+    if (consume) {
+        for (auto &g : s->glue_events) s->glue_pool.push_back(g.second);
+        s->glue_events.clear();
+    }
+    if (ms_out) for (int i = 0; i < 3; ++i) ms_out[i] = acc[i];
+    if (n_out) for (int i = 0; i < 3; ++i) n_out[i] = n[i];
+    return GLM_OK;
+}
+
 int glm_device_count(int *out) {
     GLM_CUDA_TRY(cudaGetDeviceCount(out));
     return GLM_OK;
@@ -145,6 +165,9 @@ int glm_solver_destroy(glm_solver *s) {
     for (auto &ev : s->events) s->event_pool.push_back(ev);
     for (auto &ev : s->event_pool)
         for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    for (auto &g : s->glue_events) s->glue_pool.push_back(g.second);
+    for (auto &ev : s->glue_pool)
+        for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);
     cudaSetDevice(prev);
     delete s;
     return GLM_OK;

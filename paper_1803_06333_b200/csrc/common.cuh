@@ -36,7 +36,7 @@ struct SolveState {
     int32_t epoch_blocks;     // blocks of the last epoch kernel (g-sum partials)
     double gsum_acc;          // sum_j g(base_j + delta_j) of the accepted state
     uint32_t block_counter;   // last-block-done counter for reductions
-    int32_t _pad;
+    uint32_t turn;            // barrier generation of glm_round_turn (peer.cu)
     // chunked (out-of-core) mode, pipeline.py:158-197: the chunk being solved
     // (a sequence number over epochs x chunks; -1 before the first) and the
     // g-sum of its coordinates in the accepted state.

@@ -56,7 +56,7 @@ __device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
 __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     SolveState *st, const double *delta0, const double *delta1, const double *view0,
     const double *view1, const double *lin, double quad, int64_t m, int64_t d, double *alpha,
-    int box, double *dv, int64_t *ctl) {
+    int box, double *dv, int64_t *ctl, int next_known, uint64_t next_state) {
     __shared__ int s_last;
     const int dc = st->dc;
     const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
@@ -73,12 +73,17 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     }
     for (int64_t r = tid; r < d; r += nth) out[r] = (V[r] - lin[r]) / quad;
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const uint64_t g = warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
+        // the host knows the next state when every solve runs exactly one
+        // attempt; else jump by the attempts this solve consumed
+        const uint64_t g = next_known ? next_state
+                                      : warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
         if (threadIdx.x == 0) st->gen_next = g;
     }
     __syncthreads();
     if (threadIdx.x == 0) {     // the block's writes (observed through the barrier)
-        __threadfence_system(); // before its arrival; the last block then releases
+        __threadfence();        // before its arrival (GPU scope: peers read this
+                                // memory through this GPU's L2); the last block
+                                // then releases at system scope, cumulatively
         s_last = atomicAdd(reinterpret_cast<unsigned long long *>(ctl + 2), 1ull) ==
                  (unsigned long long)(gridDim.x - 1);
     }
@@ -185,17 +190,212 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
     }
 }
 
+
+// ---------------------------------------------------------------- turn
+// One kernel between two epochs (GLM_FLAG_TURN solves: one attempt each):
+//   P1  the attempt's value G and the damping decision (value_kernel mode 1)
+//   P2  finalize: alpha += delta, Delta v -> own exchange buffer, publish
+//   P3  wait for every rank's Delta v, then the next round's start
+//       (round_start_kernel mode 2)
+// P1 -> P2 is a grid barrier on st->turn (the deciding block bumps it), P2 ->
+// P3 is the ranks' publication flags (ours is released only after all our
+// blocks finished P2).  Blocks spin only on work that finishes independently
+// of them and the grid is small (2 blocks per SM), so every block becomes
+// resident.  Replaces value + finalize + round start: three kernel launches,
+// ramps and tails per round become one.
+struct TurnParams {
+    SolveState *st;
+    double *view0, *view1;
+    const double *delta0, *delta1;
+    double *partials;          // [blocks][3]
+    const double *gpart;
+    double quad;
+    double *cnst;              // this round's const in, the next round's out
+    int64_t m, d;
+    double *alpha;
+    int box, next_known;
+    uint64_t next_state;
+    int world;
+    double *const *bufs;
+    int64_t *const *flags;
+    int64_t *ctl;
+    double *dv_own;
+    int kind;
+    double lam;
+    const double *tgt;
+    double *v, *grad, *lin, *out_fv;
+    double K, L;
+    int epochs;
+    double *scratch;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) {
+    __shared__ double sm[96];
+    __shared__ int s_last;
+    __shared__ uint32_t s_turn0;
+    __shared__ int64_t s_R;
+    __shared__ int s_dc, s_vw;
+    SolveState *st = p.st;
+    volatile SolveState *vst = st;
+    if (threadIdx.x == 0) {
+        s_turn0 = vst->turn;
+        s_R = p.ctl[0];
+    }
+    __syncthreads();
+    const bool active = !vst->done;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    // ---- P1: value of the attempt
+    {
+        const double *V = vst->vw ? p.view1 : p.view0;
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (active)
+            for (int64_t r = tid; r < p.d; r += nth) {
+                const double x = V[r], l = p.lin[r];
+                if (!isfinite(x)) acc[2] += 1.0;
+                const double u = x - l;
+                acc[1] += l * u + 0.5 * u * u;
+            }
+        block_sum<3>(acc, sm);
+        if (threadIdx.x == 0) {
+            p.partials[blockIdx.x * 3 + 1] = acc[1];
+            p.partials[blockIdx.x * 3 + 2] = acc[2];
+            __threadfence();
+            s_last = atomicAdd(&st->block_counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            double tot[3] = {0.0, 0.0, 0.0};
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+                tot[1] += __ldcg(p.partials + b * 3 + 1);
+                tot[2] += __ldcg(p.partials + b * 3 + 2);
+            }
+            double gs[1] = {0.0};
+            if (active) {
+                const int eb = vst->epoch_blocks;
+                for (int b = threadIdx.x; b < eb; b += blockDim.x) gs[0] += __ldcg(p.gpart + b);
+            }
+            block_sum<3>(tot, sm);
+            block_sum<1>(gs, sm);
+            if (threadIdx.x == 0) {
+                st->block_counter = 0;
+                if (active) decide_attempt(st, *p.cnst + tot[1] / p.quad + gs[0], gs[0], tot[2], 0);
+                __threadfence();
+                atomicAdd(&st->turn, 1u);
+            }
+        }
+        if (threadIdx.x == 0) {
+            while (ld_acquire_gpu_u32(&st->turn) == s_turn0) __nanosleep(32);
+            s_dc = vst->dc;
+            s_vw = vst->vw;
+        }
+        __syncthreads();
+    }
+    // ---- P2: finalize + publish
+    {
+        const int dc = s_dc;
+        const double *dl = dc < 0 ? nullptr : (dc ? p.delta1 : p.delta0);
+        const double *V = s_vw ? p.view1 : p.view0;
+        double *out = p.dv_own + ((s_R + 1) & 1) * p.d;
+        if (dl) {
+            if (p.box)
+                for (int64_t j = tid; j < p.m; j += nth)
+                    p.alpha[j] = fmin(1.0, fmax(0.0, p.alpha[j] + __ldcg(dl + j)));
+            else
+                for (int64_t j = tid; j < p.m; j += nth) p.alpha[j] += __ldcg(dl + j);
+        }
+        for (int64_t r = tid; r < p.d; r += nth) out[r] = (__ldcg(V + r) - p.lin[r]) / p.quad;
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            const uint64_t g = p.next_known
+                                   ? p.next_state
+                                   : warp_jump(vst->gen_state, (uint64_t)vst->attempts * (uint64_t)p.m);
+            if (threadIdx.x == 0) st->gen_next = g;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl + 2), 1ull) ==
+                     (unsigned long long)(gridDim.x - 1);
+            if (s_last) {
+                p.ctl[2] = 0;
+                __threadfence_system();
+                st_release_sys(p.ctl, s_R + 1);
+            }
+        }
+    }
+    // ---- P3: every rank's Delta v, then the next round's start
+    const int64_t R = s_R + 1;
+    if (threadIdx.x == 0)
+        for (int j = 0; j < p.world; ++j)
+            while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
+    __syncthreads();
+    const int64_t off = (R & 1) * p.d;
+    double acc[1] = {0.0};
+    const bool dual = kind_is_dual(p.kind);
+    for (int64_t r = tid; r < p.d; r += nth) {
+        double s = 0.0;                           // canonical_sum: ascending rank order
+        for (int j = 0; j < p.world; ++j) s += __ldcg(p.bufs[j] + off + r);
+        const double x = p.v[r] + s;
+        p.v[r] = x;
+        double f, g;
+        if (dual) {
+            f = x * x;
+            g = x / p.lam;
+        } else {
+            f_terms(p.kind, p.lam, p.tgt[r], x, f, g);
+            if (p.kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;
+        }
+        acc[0] += f;
+        p.grad[r] = g;
+        p.lin[r] = g;
+        p.view0[r] = g;
+        p.view1[r] = g;
+    }
+    if (!reduce_last<1>(acc, p.scratch)) return;
+    double f = acc[0];
+    if (dual) f = f / (2.0 * p.lam);
+    else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+    *p.out_fv = f;
+    const double cn = (f / p.K + 0.0) / p.L;
+    *p.cnst = cn;
+    p.ctl[1] = R;
+    if (st->status != GLM_OK) return;          // keep a solver error visible to the host
+    const double G0 = cn + st->gsum_acc;       // begin_kernel with reuse_gsum, reset damping
+    st->value = G0;
+    st->initial = G0;
+    st->gen_state = st->gen_next;
+    st->damping = 1.0;
+    st->epochs_target = p.epochs;
+    st->epochs_run = 0;
+    st->retries = 0;
+    st->plateaued = 0;
+    st->attempts = 0;
+    st->status = GLM_OK;
+    st->done = 0;
+    st->dc = -1;
+    st->vw = 0;
+    st->epoch_blocks = 0;
+}
+
 __global__ void peer_consume_kernel(int64_t *ctl) { ctl[1] = ctl[0]; }
 
 int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, int64_t m,
-                  int64_t d, double *alpha, int box, cudaStream_t stream) {
+                  int64_t d, double *alpha, int box, int next_known, uint64_t next_state,
+                  cudaStream_t stream) {
     if (pr->d != d) return glm_set_error(GLM_USAGE, "peer exchange sized for another d");
     count_launch();
     int64_t blocks = ((m > d ? m : d) + 4 * PEER_THREADS - 1) / (4 * PEER_THREADS);
     blocks = blocks < 1 ? 1 : (blocks > 8 * NUM_SMS ? 8 * NUM_SMS : blocks);
     peer_finalize_kernel<<<(int)blocks, PEER_THREADS, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], lin, quad, m, d, alpha, box,
-        pr->dv, pr->ctl);
+        pr->dv, pr->ctl, next_known, next_state);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
@@ -330,9 +530,67 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
     a.view1 = s ? s->view[1] : nullptr;
     a.epochs = epochs;
     a.scratch = scratch;
+    const bool timed = s && s->timing;
+    if (timed) {
+        int rc = glue_begin(s, 1, (cudaStream_t)stream);
+        if (rc) return rc;
+    }
     count_launch();
     round_start_kernel<<<PEER_BLOCKS, PEER_THREADS, 0, (cudaStream_t)stream>>>(a);
     GLM_CUDA_TRY(cudaGetLastError());
+    if (timed) return glue_end(s, (cudaStream_t)stream);
+    return GLM_OK;
+}
+
+int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad,
+                   double *cnst, double *alpha, int64_t m, const double *target, double *v,
+                   int64_t d, double *grad, double *lin, double *out_fv, double n_nodes,
+                   double n_devices, int epochs, double *scratch, void *stream) {
+    if (!p || !s || !cnst || !alpha || !v || !grad || !lin || !out_fv || !scratch)
+        return glm_set_error(GLM_USAGE, "null argument to glm_round_turn");
+    if (p->d != d || d > s->max_rows || m > s->max_coords)
+        return glm_set_error(GLM_USAGE, "glm_round_turn sizes do not match");
+    TurnParams a{};
+    a.st = s->st;
+    a.view0 = s->view[0];
+    a.view1 = s->view[1];
+    a.delta0 = s->delta[0];
+    a.delta1 = s->delta[1];
+    a.partials = s->partials;
+    a.gpart = s->gpart;
+    a.quad = quad;
+    a.cnst = cnst;
+    a.m = m;
+    a.d = d;
+    a.alpha = alpha;
+    a.box = kind == GLM_DUAL_L2_SVM ? 1 : 0;
+    a.next_known = s->host_known ? 1 : 0;
+    a.next_state = s->host_gen;
+    a.world = p->world;
+    a.bufs = p->bufs_dev;
+    a.flags = p->flags_dev;
+    a.ctl = p->ctl;
+    a.dv_own = p->dv;
+    a.kind = kind;
+    a.lam = lam;
+    a.tgt = target;
+    a.v = v;
+    a.grad = grad;
+    a.lin = lin;
+    a.out_fv = out_fv;
+    a.K = n_nodes;
+    a.L = n_devices;
+    a.epochs = epochs;
+    a.scratch = scratch;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (s->timing) {
+        int rc = glue_begin(s, 2, st);
+        if (rc) return rc;
+    }
+    count_launch();
+    round_turn_kernel<<<PEER_BLOCKS, PEER_THREADS, 0, st>>>(a);
+    GLM_CUDA_TRY(cudaGetLastError());
+    if (s->timing) return glue_end(s, st);
     return GLM_OK;
 }
 

@@ -498,6 +498,44 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
 }
 
 // ------------------------------------------------------- value + decide
+// damped_solve's control flow after an attempt (solver.py:272-298; per chunk
+// _train_chunk, pipeline.py:180-193) for the new value G (one thread).
+__device__ __forceinline__ void decide_attempt(SolveState *st, double G, double gnew,
+                                               double nonfinite, int chunked) {
+    st->attempts += 1;
+    if (nonfinite > 0.0) {         // solver.py:279-280
+        st->status = GLM_SOLVER_ERROR;
+        st->done = 1;
+        return;
+    }
+    if (st->status != GLM_OK) {    // coordinate-level error (solver.py:160-161, 185-186)
+        st->done = 1;
+        return;
+    }
+    const double value = st->value;
+    if (G > value) {
+        st->vw ^= 1;               // restore the snapshot view; delta[dc] untouched
+        if (G - value <= PLATEAU_REL * (1.0 + fabs(value))) {
+            st->plateaued = 1;
+            st->done = 1;
+            return;
+        }
+        st->retries += 1;
+        st->damping *= 0.5;
+        if (st->damping < DAMPING_FLOOR) {
+            st->status = GLM_DIVERGENCE;
+            st->done = 1;
+        }
+        return;
+    }
+    st->value = G;
+    st->gsum_acc = gnew;
+    st->dc = st->dc == 0 ? 1 : 0;  // the buffer the epoch wrote
+    if (!chunked && st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
+    st->epochs_run += 1;
+    if (st->epochs_run >= st->epochs_target) st->done = 1;
+}
+
 struct ValueParams {
     SolveState *st;
     int mode;   // 0: initial G; 1: after an attempt; 2: chunk g-sum of the accepted state
@@ -583,41 +621,7 @@ __global__ void __launch_bounds__(VALUE_THREADS) value_kernel(ValueParams p) {
         return;
     }
     const double gnew = p.chunked ? (st->gsum_acc - st->gsum_old) + gs[0] : gs[0];
-    const double G = *p.cnst + tot[1] / p.quad + gnew;
-    // damped_solve control flow (solver.py:272-298); per chunk: _train_chunk
-    // (pipeline.py:180-193)
-    st->attempts += 1;
-    if (tot[2] > 0.0) {            // solver.py:279-280
-        st->status = GLM_SOLVER_ERROR;
-        st->done = 1;
-        return;
-    }
-    if (st->status != GLM_OK) {    // coordinate-level error (solver.py:160-161, 185-186)
-        st->done = 1;
-        return;
-    }
-    const double value = st->value;
-    if (G > value) {
-        st->vw ^= 1;               // restore the snapshot view; delta[dc] untouched
-        if (G - value <= PLATEAU_REL * (1.0 + fabs(value))) {
-            st->plateaued = 1;
-            st->done = 1;
-            return;
-        }
-        st->retries += 1;
-        st->damping *= 0.5;
-        if (st->damping < DAMPING_FLOOR) {
-            st->status = GLM_DIVERGENCE;
-            st->done = 1;
-        }
-        return;
-    }
-    st->value = G;
-    st->gsum_acc = gnew;
-    st->dc = st->dc == 0 ? 1 : 0;  // the buffer the epoch wrote
-    if (!p.chunked && st->epochs_run < MAX_EPOCH_VALUES) st->epoch_values[st->epochs_run] = G;
-    st->epochs_run += 1;
-    if (st->epochs_run >= st->epochs_target) st->done = 1;
+    decide_attempt(st, *p.cnst + tot[1] / p.quad + gnew, gnew, tot[2], p.chunked);
 }
 
 // ---------------------------------------------------------- begin / end
@@ -670,7 +674,8 @@ __global__ void snapshot_kernel(const SolveState *st, double *view0, double *vie
 __global__ void finalize_kernel(SolveState *st, const double *delta0, const double *delta1,
                                 const double *view0, const double *view1, const double *lin,
                                 double quad, int64_t m, int64_t d, double *delta_out,
-                                double *dv_out, int accumulate, int box) {
+                                double *dv_out, int accumulate, int box, int next_known = 0,
+                                uint64_t next_state = 0) {
     const int dc = st->dc;
     const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
     const double *V = st->vw ? view1 : view0;
@@ -698,7 +703,8 @@ __global__ void finalize_kernel(SolveState *st, const double *delta0, const doub
             for (int64_t r = tid; r < d; r += nth) dv_out[r] = (V[r] - lin[r]) / quad;
     }
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const uint64_t g = warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
+        const uint64_t g = next_known ? next_state
+                                      : warp_jump(st->gen_state, (uint64_t)st->attempts * (uint64_t)m);
         if (threadIdx.x == 0) st->gen_next = g;
     }
 }
@@ -918,6 +924,24 @@ static cudaError_t event_record(cudaEvent_t ev, cudaStream_t stream) {
     return cudaEventRecord(ev, stream);
 }
 
+int glue_begin(glm_solver *s, int kind, cudaStream_t stream) {
+    std::array<cudaEvent_t, 2> ev{};
+    if (!s->glue_pool.empty()) {
+        ev = s->glue_pool.back();
+        s->glue_pool.pop_back();
+    } else {
+        for (int i = 0; i < 2; ++i) GLM_CUDA_TRY(cudaEventCreate(&ev[i]));
+    }
+    GLM_CUDA_TRY(event_record(ev[0], stream));
+    s->glue_events.push_back({kind, ev});
+    return GLM_OK;
+}
+
+int glue_end(glm_solver *s, cudaStream_t stream) {
+    GLM_CUDA_TRY(event_record(s->glue_events.back().second[1], stream));
+    return GLM_OK;
+}
+
 // The prefetch branch (side stream) must rejoin `stream` before the solver's
 // scratch is reused or a graph capture ends.
 // A join retires the prefetch: its event may have been recorded inside a graph
@@ -1089,6 +1113,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     // start instead of sitting between them and the next epoch).
     const bool early = (a->flags & GLM_FLAG_PREFETCH_PERM) && s->host_known &&
                        a->max_attempts == 1 && a->epochs == 1 && m > 0;
+    // GLM_FLAG_TURN: one attempt, and glm_round_turn follows on this stream
+    const bool turn = (a->flags & GLM_FLAG_TURN) && a->max_attempts == 1 && a->epochs == 1 &&
+                      m > 0;
     const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
     auto ensure_side = [&]() -> int {
         if (!s->side) {
@@ -1142,9 +1169,11 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         }
         if (r) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[2], stream));
-        count_launch();
-        value_kernel<<<value_grid_view(d), VALUE_THREADS, 0, stream>>>(vp);
-        GLM_CUDA_TRY(cudaGetLastError());
+        if (!turn) {          // GLM_FLAG_TURN: glm_round_turn takes the value
+            count_launch();
+            value_kernel<<<value_grid_view(d), VALUE_THREADS, 0, stream>>>(vp);
+            GLM_CUDA_TRY(cudaGetLastError());
+        }
         if (s->timing) {
             GLM_CUDA_TRY(event_record(ev[3], stream));
             s->events.push_back(ev);
@@ -1175,18 +1204,24 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         count_launch();
         empty_solve_kernel<<<1, 1, 0, stream>>>(s->st);
     }
-    if ((a->flags & GLM_FLAG_PEER_FINALIZE) && a->peer && a->accumulate && delta_out) {
+    if (turn) {
+        // value, finalize and the exchange run in glm_round_turn
+    } else if (s->timing && (rc = glue_begin(s, 0, stream))) {
+        return rc;
+    } else if ((a->flags & GLM_FLAG_PEER_FINALIZE) && a->peer && a->accumulate && delta_out) {
         // Delta v goes to this rank's peer-exchange buffer (peer.cu)
         rc = peer_finalize(s, a->peer, a->lin, a->quad, m, d, delta_out,
-                           a->kind == GLM_DUAL_L2_SVM ? 1 : 0, stream);
+                           a->kind == GLM_DUAL_L2_SVM ? 1 : 0, early ? 1 : 0, next_state, stream);
         if (rc) return rc;
     } else {
         count_launch();
         finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
             s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
-            delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0);
+            delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0, early ? 1 : 0,
+            next_state);
         GLM_CUDA_TRY(cudaGetLastError());
     }
+    if (!turn && s->timing && (rc = glue_end(s, stream))) return rc;
     s->last_epochs = a->epochs;
     s->last_m = m;
     if (early) {

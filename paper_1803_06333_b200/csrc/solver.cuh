@@ -31,6 +31,9 @@ struct glm_solver {
     bool host_known = false;              // host_gen == the device's next start state
     uint64_t host_gen = 0;
     std::vector<std::array<cudaEvent_t, 4>> events, event_pool;
+    // glue timing: {kind (0 finalize, 1 round start), start, end}
+    std::vector<std::pair<int, std::array<cudaEvent_t, 2>>> glue_events;
+    std::vector<std::array<cudaEvent_t, 2>> glue_pool;
     int last_epochs = 0;
     int64_t last_m = 0;
     const double *sq_src = nullptr;       // mean |a|^2 cache (narrow dense budget)
@@ -49,8 +52,12 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
                 cudaStream_t stream);
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
 int join_prefetch(glm_solver *s, cudaStream_t stream);
+// record the start of a timed glue kernel (returns the pair to close with glue_end)
+int glue_begin(glm_solver *s, int kind, cudaStream_t stream);
+int glue_end(glm_solver *s, cudaStream_t stream);
 int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, int64_t m,
-                  int64_t d, double *alpha, int box, cudaStream_t stream);
+                  int64_t d, double *alpha, int box, int next_known, uint64_t next_state,
+                  cudaStream_t stream);
 
 // ---- chunked (out-of-core) solves: stream.cu drives these per chunk.
 struct ChunkRecord {          // written by the close kernel into host-mapped memory

@@ -263,6 +263,7 @@ class Engine:
         # lags one round's Delta v until _flush_v() (before anything reads v).
         self.exchange = None
         self._pending = False
+        self._turn_ready = False    # the last glm_round_turn already started the next round
         if (peer_exchange and len(self.workers) == 1 and config.t2 == 1
                 and chunk_runner is None and not self.sync_solves
                 and (self.reducer is None or getattr(self.reducer, "on_cuda", False))):
@@ -300,6 +301,7 @@ class Engine:
         if self.exchange is not None:            # drop the last round's Delta v
             self.exchange.consume(self.stream)
             self._pending = False
+            self._turn_ready = False
         for (k, l), wk in self.workers.items():
             wk.gen.state = derive_seed(self.config.seed, k * self.config.devices + l)
             wk.solver.set_state(wk.gen.state, 1.0, self.stream)
@@ -337,6 +339,7 @@ class Engine:
 
     @alpha.setter
     def alpha(self, value):
+        self._turn_ready = False
         self.alpha_dev = _D().to_device(value).clone()
         for wk in self.workers.values():
             wk.gsum_ok = False
@@ -360,6 +363,7 @@ class Engine:
         if self.exchange is not None:           # a pending Delta v no longer applies
             self.exchange.consume(self.stream)
             self._pending = False
+            self._turn_ready = False
         self.v_dev[:self.d] = _D().to_device(value)
 
     @property
@@ -435,17 +439,22 @@ class Engine:
         cfg = self.config
         wk = next(iter(self.workers.values()))
         reuse = wk.gsum_ok
-        L.check(L.lib().glm_round_start(
-            self.exchange.handle, wk.solver.handle, 2 if reuse else 1, self.spec.index,
-            self.spec.lam, D.ptr(self.row_target), D.ptr(self.v_dev), self.d, D.ptr(self.grad),
-            D.ptr(self.lin), D.ptr(self.scal[0:1]), D.ptr(self.scal[1:2]), float(cfg.nodes),
-            float(cfg.devices), int(cfg.epochs), D.ptr(D.scratch(self.stream)),
-            D.sptr(self.stream)), "glm_round_start")
-        self._pending = True
+        # one attempt per round (no retry budget): the round ends in
+        # glm_round_turn, which also starts the next round
+        turn = self.retry_budget == 0 and cfg.epochs == 1 and wk.m > 0
+        if not (turn and self._turn_ready):
+            L.check(L.lib().glm_round_start(
+                self.exchange.handle, wk.solver.handle, 2 if reuse else 1, self.spec.index,
+                self.spec.lam, D.ptr(self.row_target), D.ptr(self.v_dev), self.d,
+                D.ptr(self.grad), D.ptr(self.lin), D.ptr(self.scal[0:1]), D.ptr(self.scal[1:2]),
+                float(cfg.nodes), float(cfg.devices), int(cfg.epochs),
+                D.ptr(D.scratch(self.stream)), D.sptr(self.stream)), "glm_round_start")
+            self._pending = False
         quad = cfg.sigma_bar_eff * cfg.sigma_eff * self.spec.beta
         a_slice = self.alpha_dev[wk.lo:wk.hi]
         flags = self.cache_flags | L.FLAG_PREFETCH_PERM | L.FLAG_PEER_FINALIZE | \
-            ((L.FLAG_REUSE_GSUM | L.FLAG_SKIP_BEGIN) if reuse else 0)
+            ((L.FLAG_REUSE_GSUM | L.FLAG_SKIP_BEGIN) if reuse or (turn and self._turn_ready)
+             else 0) | (L.FLAG_TURN if turn else 0)
         wk.last = wk.solver.solve(
             wk.data, self.spec, lin=self.lin, cnst=self.scal[1:2], base=a_slice, quad=quad,
             epochs=cfg.epochs, mode=self.mode, delta_out=a_slice, dv_out=None,
@@ -453,6 +462,17 @@ class Engine:
             max_attempts=cfg.epochs + self.retry_budget, group_lanes=self.group_lanes,
             max_inflight=self.max_inflight, accumulate=True, flags=flags, stream=self.stream,
             peer=self.exchange)
+        if turn:
+            L.check(L.lib().glm_round_turn(
+                self.exchange.handle, wk.solver.handle, self.spec.index, self.spec.lam, quad,
+                D.ptr(self.scal[1:2]), D.ptr(a_slice), wk.m, D.ptr(self.row_target),
+                D.ptr(self.v_dev), self.d, D.ptr(self.grad), D.ptr(self.lin),
+                D.ptr(self.scal[0:1]), float(cfg.nodes), float(cfg.devices), int(cfg.epochs),
+                D.ptr(D.scratch(self.stream)), D.sptr(self.stream)), "glm_round_turn")
+            self._turn_ready = True
+            self._pending = False
+        else:
+            self._pending = True
         wk.gsum_ok = True
         self.last_results = []
         self.stamp += 1

@@ -276,6 +276,15 @@ class DeviceSolver:
                    n.ctypes.data_as(ctypes.c_void_p)), "glm_solver_timing_read")
         return ms, int(n[0])
 
+    def timing_glue(self, consume=True):
+        """(finalize_ms, round_start_ms, turn_ms) summed, and their counts."""
+        ms = np.zeros(3)
+        n = np.zeros(3, dtype=np.int32)
+        L.check(L.lib().glm_solver_timing_glue(self.handle, ms.ctypes.data_as(ctypes.c_void_p),
+                                               n.ctypes.data_as(ctypes.c_void_p),
+                                               1 if consume else 0), "glm_solver_timing_glue")
+        return ms, n
+
     def result(self, stream=None):
         res = L.GlmSolveResult()
         ev = self.epoch_values

@@ -33,8 +33,11 @@ def _synth(n, d, k, seed):
     return g.SparseColumnMatrix(d, indptr, rows.reshape(-1).astype(np.int32), vals.reshape(-1))
 
 
+@pytest.mark.parametrize("retry_budget", [4, 0])
 @pytest.mark.parametrize("kind", ["dual_l2_logistic", "dual_l2_svm", "ridge_primal"])
-def test_fused_round_bit_identical_single_gpu(kind):
+def test_fused_round_bit_identical_single_gpu(kind, retry_budget):
+    """retry_budget 0: one attempt per round, the round ends in glm_round_turn
+    (value + finalize + exchange + next round start in one kernel)."""
     m = _synth(6_000, 900, 8, 3)
     om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
     if kind == "ridge_primal":
@@ -45,17 +48,17 @@ def test_fused_round_bit_identical_single_gpu(kind):
         tgt = None
         spec = g.ObjectiveSpec(kind, 1.0, m.n_cols, m.n_rows)
         k = 0 if kind == "dual_l2_logistic" else 1
-    cfg = g.HierarchyConfig(t1=6, seed=5, epochs=2)
+    cfg = g.HierarchyConfig(t1=6, seed=5, epochs=2 if retry_budget else 1)
     runs = []
     for peer in (False, True):
-        eng = g.Engine(m, spec, cfg, mode="sequential", sync_solves=False, retry_budget=4,
-                       peer_exchange=peer)
+        eng = g.Engine(m, spec, cfg, mode="sequential", sync_solves=False,
+                       retry_budget=retry_budget, peer_exchange=peer)
         assert (eng.exchange is not None) == peer
         runs.append(eng.train(g.StoppingCriteria(max_rounds=6)))
     np.testing.assert_array_equal(runs[0].trace.objectives(), runs[1].trace.objectives())
     np.testing.assert_array_equal(runs[0].model.alpha, runs[1].model.alpha)
     np.testing.assert_array_equal(runs[0].v, runs[1].v)
-    want = oracle.train(om, k, 1.0, target=tgt, epochs=2, seed=5, rounds=6)
+    want = oracle.train(om, k, 1.0, target=tgt, epochs=cfg.epochs, seed=5, rounds=6)
     np.testing.assert_allclose(runs[1].trace.objectives(), want["objective"], rtol=1e-10)
 
 
@@ -65,7 +68,7 @@ def test_fused_round_reset_and_graph_replay():
     m = _synth(20_000, 2_000, 10, 8)
     spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
     eng = g.Engine(m, spec, g.HierarchyConfig(seed=2, epochs=1), mode="sequential",
-                   sync_solves=False)
+                   sync_solves=False, retry_budget=0)
     for _ in range(4):
         eng.outer_round()
     v_eager, a_eager = eng.v, eng.alpha
@@ -74,7 +77,6 @@ def test_fused_round_reset_and_graph_replay():
     eng.reset()
     graph.replay()
     torch.cuda.synchronize()
-    eng._pending = True                     # the replayed rounds left their Delta v pending
     np.testing.assert_array_equal(eng.alpha, a_eager)
     np.testing.assert_array_equal(eng.v, v_eager)
 
