@@ -309,24 +309,30 @@ def ours_main(args):
     torch.cuda.synchronize()
     eng.check_solves()
     wk.solver.timing_read()                     # drop warm-up events
-    graph = None
+    graph = graph_inst = None
     launches_per_traj = None
     if args.graph:
+        # two captures of the same trajectory: the timed one without any
+        # instrumentation, and one with the library's per-kernel CUDA events
+        # (read for the roofline / breakdown, never for the step time)
         try:
             eng.reset()
-            wk.solver.timing(True)
             c0 = lib.glm_launch_count()
             graph = eng.capture(traj)
             launches_per_traj = lib.glm_launch_count() - c0
+            eng.reset()
+            wk.solver.timing(True)
+            graph_inst = eng.capture(traj)
             wk.solver.timing(False)
         except Exception as exc:   # pragma: no cover - capture unsupported
             print(f"graph capture failed ({exc!r}); timing eager rounds", file=sys.stderr)
-            graph = None
+            graph = graph_inst = None
             wk.solver.timing(False)
             wk.solver.timing_read()
             torch.cuda.synchronize()
 
-    def run_traj():
+    def run_traj(g=None):
+        g = graph if g is None else g
         eng.reset()
         if world > 1:
             torch.distributed.barrier()
@@ -334,8 +340,8 @@ def ours_main(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        if graph is not None:
-            graph.replay()
+        if g is not None:
+            g.replay()
         else:
             for _ in range(traj):
                 eng.outer_round()
@@ -349,8 +355,14 @@ def ours_main(args):
     glue_n = np.zeros(3)
     attempts = 0
     with ClockSampler(local) as clk:
-        t_w = time.perf_counter()          # keep the GPU busy while nvidia-smi starts
-        while time.perf_counter() - t_w < 0.6:
+        # keep the GPU busy while nvidia-smi starts (~0.6 s).  Every rank must run
+        # the same number of rounds (the ranks' exchange counters advance per
+        # round), so the count is agreed on, not taken from each rank's clock.
+        t_w = time.perf_counter()
+        run_traj()
+        n_warm = int(0.6 / max(time.perf_counter() - t_w, 1e-4))
+        n_warm = int(max_over_ranks(float(min(max(n_warm, 1), 200)), world))
+        for _ in range(n_warm):
             run_traj()
         if graph is None:
             wk.solver.timing_read()
@@ -359,14 +371,17 @@ def ours_main(args):
         seg_ms = 0.0
         for _ in range(n_seg):
             seg_ms += run_traj()
-            if graph is not None:
+        launches = lib.glm_launch_count() - launches0
+        inst_ms = 0.0
+        if graph_inst is not None:           # the per-kernel breakdown, after the timing
+            for _ in range(max(1, min(n_seg, 5))):
+                inst_ms += run_traj(graph_inst)
                 k_ms, k_n = wk.solver.timing_read(consume=False)
                 kern_ms += k_ms
                 attempts += k_n
                 g_ms, g_n = wk.solver.timing_glue(consume=False)
                 glue_ms += g_ms
                 glue_n += g_n
-        launches = lib.glm_launch_count() - launches0
         if graph is None:
             k_ms, attempts = wk.solver.timing_read()
             kern_ms += k_ms
@@ -398,7 +413,12 @@ def ours_main(args):
                                       "finalize_publish": glue_ms[0] / max(glue_n[0], 1),
                                       "round_start": glue_ms[1] / max(glue_n[1], 1),
                                       "round_turn": glue_ms[2] / max(glue_n[2], 1),
-                                      "step": ms_step}}
+                                      "step": ms_step,
+                                      "step_instrumented": (inst_ms / max(1, min(n_seg, 5))
+                                                            / traj if graph_inst else None),
+                                      "note": "kernel times from a second, event-instrumented "
+                                              "capture of the same trajectory; the step (and "
+                                              "value) from the uninstrumented one"}}
     # The epoch's real ceiling: every nnz is one random 8-byte gather and one
     # random f64 red into the L2-resident shared vector.  Measured live by a
     # microbenchmark doing exactly the epoch's nnz_loc gathers + reds into a

@@ -371,6 +371,9 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
                     double *out_fv, double *cnst, double n_nodes, double n_devices, int epochs,
                     double *scratch, void *stream);
 int glm_peer_destroy(glm_peer *p);
+/* Debug: glm_round_turn writes %globaltimer stamps (ns) of its phases into
+ * device u64[8]: start, decided, published, every rank seen, done (NULL: off). */
+int glm_peer_stamps(glm_peer *p, uint64_t *device_array);
 /* After a GLM_FLAG_TURN solve: the attempt's value check and damping decision,
  * alpha += delta, publish Delta v, wait for every rank's, v += their rank-order
  * sum, and the next round's model and solver start — one kernel (peer.cu).

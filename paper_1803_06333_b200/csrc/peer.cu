@@ -32,6 +32,7 @@ struct glm_peer {
     double **bufs_dev = nullptr;  // world pointers to each rank's dv (device array)
     int64_t **flags_dev = nullptr;
     std::vector<void *> opened;   // cudaIpc-opened peer allocations
+    uint64_t *stamps = nullptr;   // glm_peer_stamps: turn phase timestamps (debug)
     cudaIpcMemHandle_t handle{};
 };
 
@@ -227,7 +228,14 @@ struct TurnParams {
     double K, L;
     int epochs;
     double *scratch;
+    uint64_t *stamps;          // optional phase timestamps (globaltimer ns)
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
     uint32_t v;
@@ -235,7 +243,9 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
     return v;
 }
 
-__global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) {
+constexpr int TURN_THREADS = 512;
+
+__global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) {
     __shared__ double sm[96];
     __shared__ int s_last;
     __shared__ uint32_t s_turn0;
@@ -246,6 +256,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
     if (threadIdx.x == 0) {
         s_turn0 = vst->turn;
         s_R = p.ctl[0];
+        if (p.stamps && blockIdx.x == 0) p.stamps[0] = gtimer();
     }
     __syncthreads();
     const bool active = !vst->done;
@@ -262,8 +273,13 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
                 const double u = x - l;
                 acc[1] += l * u + 0.5 * u * u;
             }
+        if (p.stamps && blockIdx.x == 0) {
+            __syncthreads();
+            if (threadIdx.x == 0) p.stamps[5] = gtimer();
+        }
         block_sum<3>(acc, sm);
         if (threadIdx.x == 0) {
+            if (p.stamps && blockIdx.x == 0) p.stamps[6] = gtimer();
             p.partials[blockIdx.x * 3 + 1] = acc[1];
             p.partials[blockIdx.x * 3 + 2] = acc[2];
             __threadfence();
@@ -272,6 +288,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
         __syncthreads();
         if (s_last) {
             __threadfence();
+            if (p.stamps && threadIdx.x == 0) p.stamps[7] = gtimer();
             double tot[3] = {0.0, 0.0, 0.0};
             for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
                 tot[1] += __ldcg(p.partials + b * 3 + 1);
@@ -288,6 +305,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
                 st->block_counter = 0;
                 if (active) decide_attempt(st, *p.cnst + tot[1] / p.quad + gs[0], gs[0], tot[2], 0);
                 __threadfence();
+                if (p.stamps) p.stamps[1] = gtimer();
                 atomicAdd(&st->turn, 1u);
             }
         }
@@ -304,12 +322,21 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
         const double *dl = dc < 0 ? nullptr : (dc ? p.delta1 : p.delta0);
         const double *V = s_vw ? p.view1 : p.view0;
         double *out = p.dv_own + ((s_R + 1) & 1) * p.d;
-        if (dl) {
-            if (p.box)
-                for (int64_t j = tid; j < p.m; j += nth)
-                    p.alpha[j] = fmin(1.0, fmax(0.0, p.alpha[j] + __ldcg(dl + j)));
-            else
-                for (int64_t j = tid; j < p.m; j += nth) p.alpha[j] += __ldcg(dl + j);
+        if (dl) {   // 4 independent rows per thread and pass: keep loads in flight
+            for (int64_t j0 = tid; j0 < p.m; j0 += 4 * nth) {
+                double a[4], x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t j = j0 + u * nth;
+                    a[u] = j < p.m ? p.alpha[j] : 0.0;
+                    x[u] = j < p.m ? __ldcg(dl + j) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t j = j0 + u * nth;
+                    if (j < p.m) p.alpha[j] = p.box ? fmin(1.0, fmax(0.0, a[u] + x[u])) : a[u] + x[u];
+                }
+            }
         }
         for (int64_t r = tid; r < p.d; r += nth) out[r] = (__ldcg(V + r) - p.lin[r]) / p.quad;
         if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -325,16 +352,29 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
                      (unsigned long long)(gridDim.x - 1);
             if (s_last) {
                 p.ctl[2] = 0;
-                __threadfence_system();
-                st_release_sys(p.ctl, s_R + 1);
+                if (p.stamps) p.stamps[2] = gtimer();
+                if (p.world > 1) {          // peers read this flag over NVLink
+                    __threadfence_system();
+                    st_release_sys(p.ctl, s_R + 1);
+                } else {
+                    atomicExch(reinterpret_cast<unsigned long long *>(p.ctl),
+                               (unsigned long long)(s_R + 1));
+                }
             }
         }
     }
     // ---- P3: every rank's Delta v, then the next round's start
     const int64_t R = s_R + 1;
-    if (threadIdx.x == 0)
-        for (int j = 0; j < p.world; ++j)
-            while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
+    if (threadIdx.x == 0) {
+        if (p.world > 1) {
+            for (int j = 0; j < p.world; ++j)
+                while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
+        } else {
+            while ((int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl), 0ull) < R)
+                __nanosleep(32);
+        }
+    }
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[3] = gtimer();
     __syncthreads();
     const int64_t off = (R & 1) * p.d;
     double acc[1] = {0.0};
@@ -366,6 +406,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_turn_kernel(TurnParams p) 
     const double cn = (f / p.K + 0.0) / p.L;
     *p.cnst = cn;
     p.ctl[1] = R;
+    if (p.stamps) p.stamps[4] = gtimer();
     if (st->status != GLM_OK) return;          // keep a solver error visible to the host
     const double G0 = cn + st->gsum_acc;       // begin_kernel with reuse_gsum, reset damping
     st->value = G0;
@@ -491,6 +532,14 @@ int glm_peer_open(glm_peer *p, const void *handles) {
     return GLM_OK;
 }
 
+// Debug: record glm_round_turn phase timestamps (globaltimer ns) into a
+// device array of 8 u64 (start, decided, published, peers seen, done).
+int glm_peer_stamps(glm_peer *p, uint64_t *device_array) {
+    if (!p) return glm_set_error(GLM_USAGE, "null peer");
+    p->stamps = device_array;
+    return GLM_OK;
+}
+
 int glm_peer_consume(glm_peer *p, void *stream) {
     if (!p) return glm_set_error(GLM_USAGE, "null peer");
     count_launch();
@@ -582,13 +631,14 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
     a.L = n_devices;
     a.epochs = epochs;
     a.scratch = scratch;
+    a.stamps = p->stamps;
     cudaStream_t st = (cudaStream_t)stream;
     if (s->timing) {
         int rc = glue_begin(s, 2, st);
         if (rc) return rc;
     }
     count_launch();
-    round_turn_kernel<<<PEER_BLOCKS, PEER_THREADS, 0, st>>>(a);
+    round_turn_kernel<<<PEER_BLOCKS, TURN_THREADS, 0, st>>>(a);
     GLM_CUDA_TRY(cudaGetLastError());
     if (s->timing) return glue_end(s, st);
     return GLM_OK;

@@ -1119,7 +1119,11 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
     auto ensure_side = [&]() -> int {
         if (!s->side) {
-            GLM_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+            // the permutation prefetch runs at the lowest priority so the
+            // caller's round kernels (epoch, turn) get free SMs first
+            int lo = 0, hi = 0;
+            GLM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            GLM_CUDA_TRY(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, lo));
             GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
             GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
         }

@@ -317,7 +317,9 @@ class Engine:
         if self.sync_solves or self.chunk_runner is not None:
             raise ValueError("graph capture needs sync_solves=False and the device solver")
         D = _D()
-        side = torch.cuda.Stream()
+        # captured at the highest priority (kernel nodes keep their stream's
+        # priority): the round's kernels win SMs over the permutation prefetch
+        side = torch.cuda.Stream(priority=-100)
         side.wait_stream(torch.cuda.current_stream())
         D.scratch(side)                        # allocate outside the capture
         graph = torch.cuda.CUDAGraph()
