@@ -1,0 +1,187 @@
+#!/usr/bin/env python
+"""Multi-GPU runs of BASELINE configs C3 (dense SVM, examples partitioned) and
+C4 (lasso primal, features column-partitioned), one process per GPU:
+
+    python -m torch.distributed.run --nproc-per-node N tools/bench_multi.py c3|c4
+
+Each rank generates only its own partition on its GPU (the same data for any N:
+blocks are seeded by their global index), builds the engine with the NVLink
+peer exchange, and times async rounds with CUDA events (max over ranks).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1803_06333_b200 as g  # noqa: E402
+from paper_1803_06333_b200 import _lib as L  # noqa: E402
+from paper_1803_06333_b200.comm import NcclReducer  # noqa: E402
+from paper_1803_06333_b200.data import DeviceMatrix  # noqa: E402
+
+HBM = 6552.3
+
+
+def max_all(x):
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    if dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(eng, rounds, gap=True):
+    ms, rel = [], []
+    obj, gp = eng.objective_and_gap()
+    rel.append(None if gp is None or obj == 0 else gp / abs(obj))
+    for _ in range(rounds):
+        if dist.is_initialized():
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.outer_round()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(max_all(a.elapsed_time(b)))
+        eng.check_solves()
+        if gap:
+            obj, gp = eng.objective_and_gap()
+            rel.append(None if gp is None or obj == 0 else gp / abs(obj))
+        else:
+            rel.append(eng.objective_and_gap()[0])
+    return ms, rel
+
+
+def c3(args, rank, world):
+    n, d, lam = args.n, 28, args.lam
+    blocks = 8
+    per = n // blocks
+    lo_b, hi_b = rank * blocks // world, (rank + 1) * blocks // world
+    gw = torch.Generator(device="cuda").manual_seed(33)
+    w = torch.randn(d, device="cuda", dtype=torch.float64, generator=gw)
+    parts = []
+    for b in range(lo_b, hi_b):
+        gen = torch.Generator(device="cuda").manual_seed(1000 + b)
+        X = torch.randn(per, d, device="cuda", dtype=torch.float64, generator=gen)
+        X /= X.norm(dim=1, keepdim=True)
+        y = torch.where(X @ w + 0.3 * torch.randn(per, device="cuda", dtype=torch.float64,
+                                                      generator=gen) >= 0, 1.0, -1.0)
+        parts.append((X * y[:, None]).reshape(-1))
+    cm = torch.cat(parts).contiguous()
+    m_loc = (hi_b - lo_b) * per
+    dm = DeviceMatrix(d, m_loc, L.DENSE, cm)
+    n_tot = per * blocks
+    spec = g.ObjectiveSpec("dual_l2_svm", lam, n_tot, d)
+    cfg = g.HierarchyConfig(nodes=world, seed=0, epochs=1)
+    kw = dict(reducer=NcclReducer(), node_index=rank, n_total=n_tot) if world > 1 else {}
+    eng = g.Engine(dm, spec, cfg, mode="async", sync_solves=False, retry_budget=0, **kw)
+    for _ in range(2):
+        eng.outer_round()
+    eng.reset()
+    ms, rel = timed(eng, args.rounds)
+    alg = 8 * n_tot * d + 28 * n_tot
+    med = float(np.median(ms[1:]))
+    return {"config": "C3", "n_gpus": world,
+            "workload": f"dual hinge SVM, dense HIGGS-shaped {n_tot}x{d}, lambda={lam}, "
+                        f"examples partitioned over {world} GPU(s)",
+            "epoch_ms_median": med, "epochs_per_s": 1000.0 / med,
+            "coord_updates_per_s": n_tot * 1000.0 / med,
+            "hbm_frac_per_gpu": alg / world / (med * 1e-3) / 1e9 / HBM,
+            "rel_gap": rel, "round_ms": ms, "exchange": "nvlink-peer" if eng.exchange else "nccl"}
+
+
+def c4(args, rank, world):
+    n_ex, n_feat, per_col, lam = args.n_ex, args.n_feat, args.per_col, args.lam
+    blocks = 8
+    fb = n_feat // blocks
+    lo_b, hi_b = rank * blocks // world, (rank + 1) * blocks // world
+    rows_l, vals_l, coef_l = [], [], []
+    for b in range(lo_b, hi_b):
+        gen = torch.Generator(device="cuda").manual_seed(4000 + b)
+        r = torch.randint(0, n_ex - per_col + 1, (fb, per_col), device="cuda", generator=gen,
+                          dtype=torch.int64)
+        r, _ = torch.sort(r, dim=1)
+        rows_l.append((r + torch.arange(per_col, device="cuda")).to(torch.int32).reshape(-1))
+        vals_l.append(torch.randn(fb * per_col, device="cuda", dtype=torch.float64,
+                                  generator=gen))
+        c = torch.randn(fb, device="cuda", dtype=torch.float64, generator=gen)
+        c[torch.rand(fb, device="cuda", generator=gen, dtype=torch.float64) < 0.5] = 0.0
+        coef_l.append(c)
+    m_loc = (hi_b - lo_b) * fb
+    rows, vals = torch.cat(rows_l), torch.cat(vals_l)
+    indptr = torch.arange(0, m_loc * per_col + 1, per_col, device="cuda", dtype=torch.int64)
+    dm = DeviceMatrix(n_ex, m_loc, L.CSC, vals, indptr, rows, nnz=m_loc * per_col)
+    b = dm.matvec(torch.cat(coef_l)).clone()          # this partition's share of X coef
+    if world > 1:
+        dist.all_reduce(b)
+    gen = torch.Generator(device="cuda").manual_seed(4999)
+    b += 0.1 * torch.randn(n_ex, device="cuda", dtype=torch.float64, generator=gen)
+    n_tot = fb * blocks
+    spec = g.ObjectiveSpec("lasso_primal", lam, n_ex, n_tot, target=b.cpu().numpy())
+    cfg = g.HierarchyConfig(nodes=world, seed=0, epochs=1)
+    kw = dict(reducer=NcclReducer(), node_index=rank, n_total=n_tot) if world > 1 else {}
+    eng = g.Engine(dm, spec, cfg, mode="async", sync_solves=False, retry_budget=0, **kw)
+    for _ in range(2):
+        eng.outer_round()
+    eng.reset()
+    ms, objs = timed(eng, args.rounds, gap=False)
+    nnz = n_tot * per_col
+    alg = 12 * nnz + 36 * n_tot
+    med = float(np.median(ms[1:]))
+    return {"config": "C4", "n_gpus": world,
+            "workload": f"lasso (primal), sparse {n_ex}x{n_tot}, {per_col} nnz/feature, "
+                        f"lambda={lam}, features partitioned over {world} GPU(s)",
+            "epoch_ms_median": med, "epochs_per_s": 1000.0 / med,
+            "coord_updates_per_s": n_tot * 1000.0 / med,
+            "hbm_frac_per_gpu": alg / world / (med * 1e-3) / 1e9 / HBM,
+            "objective": objs, "round_ms": ms,
+            "exchange": "nvlink-peer" if eng.exchange else "nccl",
+            "exchange_bytes_per_rank_per_round": 8 * n_ex}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=("c3", "c4"))
+    ap.add_argument("--rounds", type=int, default=10)
+    ap.add_argument("--n", type=int, default=11_000_000)
+    ap.add_argument("--lam", type=float, default=None)
+    ap.add_argument("--n-ex", type=int, default=10_000_000)
+    ap.add_argument("--n-feat", type=int, default=1_000_000)
+    ap.add_argument("--per-col", type=int, default=400)
+    ap.add_argument("--out", default=None, help="append the JSON line to this file")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+    print(f"[multi r{rank}] start {args.config} world {world}", file=sys.stderr, flush=True)
+    if args.config == "c3":
+        args.lam = args.lam or 100.0
+        res = c3(args, rank, world)
+    else:
+        args.lam = args.lam or 50.0
+        res = c4(args, rank, world)
+    if rank == 0:
+        line = json.dumps(res)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "a") as fh:
+                fh.write(line + "\n")
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    os._exit(0)
+
+
+if __name__ == "__main__":
+    main()
