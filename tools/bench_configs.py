@@ -99,6 +99,28 @@ def c3(args):
     print(json.dumps(res), flush=True)
 
 
+# ------------------------------------------------------------------ C2
+def c2_modes(args):
+    """The bench workload (C2, dual logistic 1M x 100k, 40 nnz) in both modes:
+    epochs to a 1e-3 relative duality gap for the deterministic sequential
+    kernel (the parity-checked reference semantics) and the async TPA-SCD
+    kernel, i.e. the north star's "same target within the same number of
+    epochs +-10 %" at full size."""
+    import bench
+    indptr, rows, vals, _ = bench.gen_columns(0, bench.N_EX // bench.BLOCK)
+    dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
+    spec = g.ObjectiveSpec("dual_l2_logistic", bench.LAM, bench.N_EX, bench.D_FEAT)
+    res = {"config": "C2-modes", "workload": "bench.py C2 (dual L2 logistic 1M x 100k, 40 nnz)"}
+    for mode, rounds in (("async", args.rounds), ("sequential", args.seq_rounds)):
+        eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode=mode,
+                       sync_solves=(mode == "sequential"))
+        r = timed_rounds(eng, rounds)
+        res[mode] = {"epoch_ms_median": float(np.median(r["round_ms"])), "rel_gap": r["rel_gap"],
+                     "to_1e-3": r["to_target"]}
+        del eng
+    print(json.dumps(res), flush=True)
+
+
 # ------------------------------------------------------------------ C1
 def c1(args):
     """ridge_primal, dense 20k examples x 500 features (coordinates = features)."""
@@ -254,7 +276,7 @@ def c5(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=("c1", "c3", "c4", "c5"))
+    ap.add_argument("config", choices=("c1", "c2", "c3", "c4", "c5"))
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--lam", type=float, default=None)
     ap.add_argument("--rounds", type=int, default=10)
@@ -273,6 +295,8 @@ def main():
         c3(args)
     elif args.config == "c1":
         c1(args)
+    elif args.config == "c2":
+        c2_modes(args)
     elif args.config == "c4":
         args.lam = args.lam or 50.0
         c4(args)
