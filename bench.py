@@ -75,6 +75,19 @@ def gen_columns(lo_block, hi_block):
     return indptr, rows, vals, y
 
 
+def test_examples():
+    """The held-out 25 %: blocks 8 and 9 of the same generator, unfolded
+    (example-major, raw features) with their labels."""
+    from paper_1803_06333_b200.data import DeviceMatrix
+    w = planted_w()
+    parts = [gen_block(b, w) for b in (N_EX // BLOCK, N_EX // BLOCK + 1)]
+    rows = np.concatenate([p[0] for p in parts])
+    y = np.concatenate([p[2] for p in parts])
+    vals = np.concatenate([p[1] for p in parts]) * np.repeat(y, NNZ)   # undo the label fold
+    indptr = np.arange(0, len(y) * NNZ + 1, NNZ, dtype=np.int64)
+    return DeviceMatrix.from_csc(D_FEAT, indptr, rows, vals), y
+
+
 # ------------------------------------------------------------- utilities
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -267,6 +280,7 @@ def ours_main(args):
     from paper_1803_06333_b200.comm import NcclReducer
     from paper_1803_06333_b200.data import DeviceMatrix
     from paper_1803_06333_b200.solver import device_solve_host
+    from paper_1803_06333_b200 import modelio
 
     n_blocks = N_EX // BLOCK
     if n_blocks % world:
@@ -448,6 +462,22 @@ def ours_main(args):
         ttt = {"seconds": time.perf_counter() - t0, "epochs": rounds,
                "target": "duality gap <= 1e-3 * |F| (certifies relative suboptimality)",
                "final_gap": gap, "final_objective": obj, "includes_gap_checks": True}
+        # held-out test loss (PAPER.md:178 75/25 split: 250k more examples of the
+        # same distribution), scored like cmd_predict --eval (w = v / lambda,
+        # modelio.py:57-95): at the 1e-3 target and after converging further
+        test = test_examples()
+        ev_t = modelio.evaluate(test[0], eng2.v / LAM, test[1])
+        more = 0
+        while gap > 1e-9 * abs(obj) and more < 100:
+            eng2.outer_round()
+            more += 1
+            obj, gap = eng2.objective_and_gap()
+        ev_c = modelio.evaluate(test[0], eng2.v / LAM, test[1])
+        ttt["test_loss"] = {"examples": int(test[0].n_cols),
+                            "logloss_at_target": ev_t["logloss"],
+                            "accuracy_at_target": ev_t["accuracy"],
+                            "logloss_converged": ev_c["logloss"],
+                            "converged_epochs": rounds + more, "converged_rel_gap": gap / abs(obj)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
