@@ -255,11 +255,13 @@ def config_block(world):
                         "lambda=1",
             "n_examples": N_EX, "n_features": D_FEAT, "nnz_per_example": NNZ,
             "nnz": N_EX * NNZ, "lambda": LAM, "epochs_per_round": 1,
-            "parallelism": f"CoCoA K={world} (one rank per GPU, NCCL Delta-v allreduce)",
-            "solver": "async TPA-SCD (group-per-coordinate, red.global.add.f64)",
+            "parallelism": f"CoCoA K={world} (one rank per GPU; Delta v exchanged over NVLink "
+                           f"peer memory in rank order, fused with the round turn kernel)",
+            "solver": "async TPA-SCD (4 lanes x 10 registers per 40-nnz coordinate, "
+                      "red.global.add.f64 scatter), one attempt per round",
             "l2_flush": "inputs (480 MB matrix) larger than the 126 MB L2",
             "timed_region": "fresh trajectories of --traj epochs from alpha0 (resets untimed), "
-                            "each replayed as one CUDA graph"}
+                            "each replayed as one CUDA graph (no instrumentation events)"}
 
 
 # ------------------------------------------------------------ GPU arm
