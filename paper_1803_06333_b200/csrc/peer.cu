@@ -96,6 +96,23 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     }
 }
 
+// sum_j bufs[j][i] in ascending rank order (canonical_sum's bits): the (remote,
+// NVLink) loads of up to 8 ranks are issued together, then added in order.
+__device__ __forceinline__ double rank_sum(double *const *bufs, int world, int64_t i) {
+    double s = 0.0;
+    if (world <= 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = j < world ? __ldcg(bufs[j] + i) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < world) s += x[j];
+        return s;
+    }
+    for (int j = 0; j < world; ++j) s += __ldcg(bufs[j] + i);
+    return s;
+}
+
 struct RoundStart {
     int mode;                  // 0 apply pending Delta v only; 1 + model; 2 + solve start
     int kind;
@@ -136,9 +153,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
     for (int64_t r = tid; r < p.d; r += nth) {
         double x = p.v[r];
         if (apply) {
-            double s = 0.0;                       // canonical_sum: ascending rank order
-            for (int j = 0; j < p.world; ++j) s += __ldcg(p.bufs[j] + off + r);
-            x += s;
+            x += rank_sum(p.bufs, p.world, off + r);
             p.v[r] = x;
         }
         if (p.mode == 0) continue;
@@ -235,6 +250,12 @@ __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const int64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
@@ -366,12 +387,21 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     // ---- P3: every rank's Delta v, then the next round's start
     const int64_t R = s_R + 1;
     if (threadIdx.x == 0) {
-        if (p.world > 1) {
-            for (int j = 0; j < p.world; ++j)
-                while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
+        if (blockIdx.x == 0) {
+            // one poller per rank reads the peers' flags over NVLink, then
+            // releases a local "every rank published R" word (ctl[3]) that the
+            // other blocks poll in this GPU's L2
+            if (p.world > 1) {
+                for (int j = 0; j < p.world; ++j)
+                    while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
+            } else {
+                while ((int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl), 0ull) < R)
+                    __nanosleep(32);
+            }
+            __threadfence();
+            atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 3), (unsigned long long)R);
         } else {
-            while ((int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl), 0ull) < R)
-                __nanosleep(32);
+            while ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) < R) __nanosleep(32);
         }
     }
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[3] = gtimer();
@@ -380,8 +410,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     double acc[1] = {0.0};
     const bool dual = kind_is_dual(p.kind);
     for (int64_t r = tid; r < p.d; r += nth) {
-        double s = 0.0;                           // canonical_sum: ascending rank order
-        for (int j = 0; j < p.world; ++j) s += __ldcg(p.bufs[j] + off + r);
+        const double s = rank_sum(p.bufs, p.world, off + r);
         const double x = p.v[r] + s;
         p.v[r] = x;
         double f, g;

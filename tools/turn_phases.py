@@ -1,26 +1,45 @@
-"""Phase timestamps of glm_round_turn on the C2 workload (debug)."""
+"""Phase timestamps of glm_round_turn on the C2 workload (debug); world >= 1
+under torchrun. Prints, per rank, the median µs of: P1 decide | P2 publish |
+wait for every rank | P3 round start | block-0 view loads | block-0 reduced |
+last block starts its fold."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import torch.distributed as dist
 import bench
 import paper_1803_06333_b200 as g
 from paper_1803_06333_b200 import _lib as L
+from paper_1803_06333_b200.comm import NcclReducer
 from paper_1803_06333_b200.data import DeviceMatrix
-torch.cuda.set_device(0)
-torch.cuda.set_stream(torch.cuda.Stream(priority=-100 if os.environ.get("HIPRI") else 0))
-indptr, rows, vals, y = bench.gen_columns(0, bench.N_EX // bench.BLOCK)
+world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+if world > 1:
+    dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+per = (bench.N_EX // bench.BLOCK) // world
+indptr, rows, vals, y = bench.gen_columns(rank * per, (rank + 1) * per)
 dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
 spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, bench.N_EX, bench.D_FEAT)
-eng = g.Engine(dm, spec, g.HierarchyConfig(t1=10**6, seed=0, epochs=1), mode="async",
-               sync_solves=False, retry_budget=0, cache_flags=1)
+kw = dict(reducer=NcclReducer(), node_index=rank, n_total=bench.N_EX) if world > 1 else {}
+eng = g.Engine(dm, spec, g.HierarchyConfig(nodes=world, t1=10**6, seed=0, epochs=1),
+               mode="async", sync_solves=False, retry_budget=0, cache_flags=1, **kw)
 st = torch.zeros(8, dtype=torch.int64, device="cuda")
 L.check(L.lib().glm_peer_stamps(eng.exchange.handle, st.data_ptr()), "stamps")
 for _ in range(5):
     eng.outer_round()
 ph = []
-for _ in range(30):
+for _ in range(40):
     eng.outer_round()
     torch.cuda.synchronize()
     s = st.cpu().numpy().astype(np.int64)
     ph.append(np.concatenate([np.diff(s[:5]), [s[5] - s[0], s[6] - s[0], s[7] - s[0]]]) / 1e3)
-print("us: P1 decide | P2 publish | wait peers | P3 round start | blk0 view loads | blk0 reduced | last block starts ->", np.median(ph, axis=0))
+med = torch.tensor(np.median(ph, axis=0), device="cuda")
+out = [torch.zeros_like(med) for _ in range(world)]
+if world > 1:
+    dist.all_gather(out, med)
+else:
+    out = [med]
+if rank == 0:
+    for r, o in enumerate(out):
+        print(f"rank {r}:", np.round(o.cpu().numpy(), 2), flush=True)
+sys.stdout.flush()
+os._exit(0)
