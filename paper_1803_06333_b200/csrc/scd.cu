@@ -220,10 +220,9 @@ struct NarrowCol {
 };
 
 template <int R>
-__device__ __forceinline__ void narrow_load(const EpochParams &p, const double *dcur, int64_t k,
-                                            NarrowCol<R> &c) {
+__device__ __forceinline__ void narrow_load_j(const EpochParams &p, const double *dcur, int j,
+                                              NarrowCol<R> &c) {
     const int lane = threadIdx.x & 31;
-    const int j = __ldg(p.perm + k);
     c.j = j;
     const double *col = p.vals + (int64_t)j * p.d;
 #pragma unroll
@@ -235,6 +234,12 @@ __device__ __forceinline__ void narrow_load(const EpochParams &p, const double *
     c.dj = dcur ? dcur[j] : 0.0;
     c.s = __ldg(p.sq + j);
     c.y = p.y ? __ldg(p.y + j) : 0.0;
+}
+
+template <int R>
+__device__ __forceinline__ void narrow_load(const EpochParams &p, const double *dcur, int64_t k,
+                                            NarrowCol<R> &c) {
+    narrow_load_j<R>(p, dcur, __ldg(p.perm + k), c);
 }
 
 __device__ __forceinline__ double warp_allsum(double v) {
@@ -348,20 +353,37 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
     const int64_t per_cta = (int64_t)nwarp * per_phase;
     const int64_t stride = (int64_t)gridDim.x * per_cta;
-    NarrowCol<R> nx;
-    {
-        const int64_t kb0 = (int64_t)blockIdx.x * per_cta + (int64_t)warp * per_phase;
-        if (kb0 < p.m) narrow_load<R>(p, dcur, kb0, nx);
-    }
+    double prev_old = 0.0, prev_x = 0.0;   // row threadIdx.x: the last publish
+    bool have_prev = false;
+    // This warp's coordinates: position t -> k(t) = base + (t / P) * stride +
+    // t % P.  Two-stage software pipeline: the permutation entry of t + 2 and
+    // the column of t + 1 are in flight while t is stepped (the column load
+    // depends on the permutation load, so one stage alone would leave both
+    // latencies on the critical path of a short phase).
+    // position -> coordinate index, advanced without divisions: inside a
+    // phase k + 1, at its end the same slot of the next phase (k - i + stride)
+    struct Pos {
+        int64_t k;
+        int i;
+    };
+    auto adv = [&](Pos q) -> Pos {
+        return q.i + 1 < per_phase ? Pos{q.k + 1, q.i + 1} : Pos{q.k - q.i + stride, 0};
+    };
+    Pos p0{(int64_t)blockIdx.x * per_cta + (int64_t)warp * per_phase, 0};
+    Pos p1 = adv(p0), p2 = adv(p1);
+    NarrowCol<R> cur;
+    int jn = 0;
+    if (p0.k < p.m) narrow_load<R>(p, dcur, p0.k, cur);
+    if (p1.k < p.m) jn = __ldg(p.perm + p1.k);
     for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m; k0 += stride) {
-        const int64_t kb = k0 + (int64_t)warp * per_phase;
-        const int64_t ke = min(kb + per_phase, p.m);
-        for (int64_t k = kb; k < ke; ++k) {
-            const NarrowCol<R> c = nx;
-            // prefetch the next coordinate of this warp, across the phase
-            // boundary too (the column stream never waits on the fold)
-            if (k + 1 < ke) narrow_load<R>(p, dcur, k + 1, nx);
-            else if (kb + stride < p.m) narrow_load<R>(p, dcur, kb + stride, nx);
+        for (int ii = 0; ii < per_phase; ++ii) {
+            if (p0.k >= p.m) break;
+            const NarrowCol<R> c = cur;
+            if (p1.k < p.m) narrow_load_j<R>(p, dcur, jn, cur);
+            if (p2.k < p.m) jn = __ldg(p.perm + p2.k);
+            p0 = p1;
+            p1 = p2;
+            p2 = adv(p2);
             double acc = 0.0;
 #pragma unroll
             for (int i = 0; i < R; ++i) acc += c.a[i] * (snap[lane + 32 * i] + pend[i]);
@@ -383,16 +405,23 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
                 for (int i = 0; i < R; ++i) pend[i] += f * c.a[i];
             }
         }
-        // phase end: fold the warps' pendings, publish, refresh the snapshot
+        // phase end: fold the warps' pendings and publish them.  The publish's
+        // returned value is consumed one phase later (thread r owns row r), so
+        // the atomic round trip overlaps the next phase's coordinates; the
+        // snapshot gets the CTA's own contributions at once and the other
+        // CTAs' one phase late.
 #pragma unroll
         for (int i = 0; i < R; ++i)
             if (pend[i] != 0.0) atomicAdd(&fold[lane + 32 * i], pend[i]);
         __syncthreads();
-        for (int r = threadIdx.x; r < p.d; r += blockDim.x) {
+        if (threadIdx.x < p.d) {
+            const int r = threadIdx.x;
             const double x = fold[r];
-            const double old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
-            snap[r] = old + x;
             fold[r] = 0.0;
+            snap[r] = have_prev ? prev_old + prev_x + x : snap[r] + x;
+            prev_old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
+            prev_x = x;
+            have_prev = true;
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) pend[i] = 0.0;

@@ -84,7 +84,7 @@ def c3(args):
     alg = 8 * n * d + 28 * n
     for mode in ("async", "sequential") if args.seq_rounds > 0 else ("async",):
         eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode=mode,
-                       sync_solves=(mode == "sequential"))
+                       sync_solves=(mode == "sequential"), max_inflight=args.inflight)
         rounds = args.rounds if mode == "async" else args.seq_rounds
         r = timed_rounds(eng, rounds)
         ms = float(np.median(r["round_ms"]))
@@ -287,6 +287,7 @@ def main():
     ap.add_argument("--n-ex", type=int, default=10_000_000)
     ap.add_argument("--n-feat", type=int, default=1_000_000)
     ap.add_argument("--per-col", type=int, default=400)
+    ap.add_argument("--inflight", type=int, default=0, help="async in-flight budget (0 = auto)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     if args.config == "c3":
