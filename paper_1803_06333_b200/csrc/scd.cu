@@ -268,11 +268,15 @@ __global__ void __launch_bounds__(32) scd_seq_narrow(EpochParams p) {
     }
     const int kind = p.kind;
     double gacc = 0.0;
+    // two-stage pipeline: permutation entry k + 2 and column k + 1 in flight
     NarrowCol<R> nx;
+    int jn = 0;
     if (p.m > 0) narrow_load<R>(p, dcur, 0, nx);
+    if (p.m > 1) jn = __ldg(p.perm + 1);
     for (int64_t k = 0; k < p.m; ++k) {
         const NarrowCol<R> c = nx;
-        if (k + 1 < p.m) narrow_load<R>(p, dcur, k + 1, nx);
+        if (k + 1 < p.m) narrow_load_j<R>(p, dcur, jn, nx);
+        if (k + 2 < p.m) jn = __ldg(p.perm + k + 2);
         double acc = 0.0;
 #pragma unroll
         for (int i = 0; i < R; ++i) acc += c.a[i] * v[i];
