@@ -13,6 +13,27 @@
 
 namespace glm {
 
+// 128-bit accesses over [lo, hi) of an f64 array by `width` cooperating lanes:
+// a scalar head up to 16-byte alignment, a double2 body, a scalar tail;
+// f(q, x) for every element (each element exactly once).
+template <class F>
+__device__ __forceinline__ void span_f64(const double *a, int64_t lo, int64_t hi, int lane,
+                                         int width, F f) {
+    int64_t q = lo;
+    if (q < hi && (reinterpret_cast<uintptr_t>(a + q) & 15)) {
+        if (lane == 0) f(q, __ldg(a + q));
+        ++q;
+    }
+    const int64_t np = (hi - q) >> 1;
+    const double2 *a2 = reinterpret_cast<const double2 *>(a + q);
+    for (int64_t t = lane; t < np; t += width) {
+        const double2 v = __ldg(a2 + t);
+        f(q + 2 * t, v.x);
+        f(q + 2 * t + 1, v.y);
+    }
+    if (q + 2 * np < hi && lane == width - 1) f(hi - 1, __ldg(a + hi - 1));
+}
+
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(256) colwise_kernel(int op, int64_t n, int64_t d,
                                                       const int64_t *indptr,
@@ -32,11 +53,10 @@ __global__ void __launch_bounds__(256) colwise_kernel(int op, int64_t n, int64_t
             else { lo = indptr[j]; hi = indptr[j + 1]; }
         }
         double acc = 0.0;
-        for (int64_t q = lo + gl; q < hi; q += G) {
-            const double x = vals[q];
+        span_f64(vals, lo, hi, gl, G, [&](int64_t q, double x) {
             if (op == 0) acc += x * x;
-            else acc += x * w[DENSE ? (int)(q - lo) : rows[q]];
-        }
+            else acc += x * w[DENSE ? (int)(q - lo) : __ldg(rows + q)];
+        });
         acc = group_sum<G>(acc);
         if (valid && gl == 0) out[j] = acc;
     }
@@ -139,21 +159,48 @@ int launch_matvec(const glm_matrix *A, const double *x, double *out, cudaStream_
 __global__ void expand_cols_kernel(const int64_t *indptr, int64_t n, int32_t *col_of,
                                    uint32_t *keys, const int32_t *rows, int32_t *pos,
                                    int64_t nnz) {
-    // one thread per column writes its column id over its entries
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x)
-        for (int64_t q = indptr[j]; q < indptr[j + 1]; ++q) col_of[q] = (int32_t)j;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x) {
+    // a warp per column writes its column id over its entries (coalesced)
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp; j < n; j += nwarps) {
+        const int64_t lo = __ldg(indptr + j), hi = __ldg(indptr + j + 1);
+        for (int64_t q = lo + lane; q < hi; q += 32) col_of[q] = (int32_t)j;
+    }
+    // keys = rows, pos = iota: 128-bit loads and stores (the arrays are
+    // allocation-aligned), scalar tail
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = nnz >> 2;
+    const int4 *r4 = reinterpret_cast<const int4 *>(rows);
+    for (int64_t t = tid; t < n4; t += nth) {
+        const int4 r = __ldg(r4 + t);
+        reinterpret_cast<uint4 *>(keys)[t] = make_uint4((uint32_t)r.x, (uint32_t)r.y,
+                                                         (uint32_t)r.z, (uint32_t)r.w);
+        const int32_t q = (int32_t)(4 * t);
+        reinterpret_cast<int4 *>(pos)[t] = make_int4(q, q + 1, q + 2, q + 3);
+    }
+    for (int64_t q = 4 * n4 + tid; q < nnz; q += nth) {
         keys[q] = (uint32_t)rows[q];
         pos[q] = (int32_t)q;
     }
 }
 
 __global__ void row_count_kernel(const int32_t *rows, int64_t nnz, int64_t *counts) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(reinterpret_cast<unsigned long long *>(counts + rows[q] + 1), 1ULL);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = nnz >> 2;          // rows is allocation-aligned: int4 loads
+    auto add = [&](int32_t r) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(counts + r + 1), 1ULL);
+    };
+    for (int64_t t = tid; t < n4; t += nth) {
+        const int4 r = __ldg(reinterpret_cast<const int4 *>(rows) + t);
+        add(r.x);
+        add(r.y);
+        add(r.z);
+        add(r.w);
+    }
+    for (int64_t q = 4 * n4 + tid; q < nnz; q += nth) add(rows[q]);
 }
 
 __global__ void zero_i64_kernel(int64_t *p, int64_t n) {
@@ -316,10 +363,29 @@ __global__ void scale_kernel(const int64_t *indptr, int64_t n, int64_t d, int de
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // 128-bit loads and stores when vals and out share their 16-byte phase
+    const bool paired = ((reinterpret_cast<uintptr_t>(vals) ^ reinterpret_cast<uintptr_t>(out)) &
+                         15) == 0;
     for (int64_t j = warp; j < n; j += nwarps) {
         const int64_t lo = dense ? j * d : indptr[j], hi = dense ? lo + d : indptr[j + 1];
         const double sc = scales[j];
-        for (int64_t q = lo + lane; q < hi; q += 32) out[q] = vals[q] * sc;
+        if (!paired) {
+            for (int64_t q = lo + lane; q < hi; q += 32) out[q] = vals[q] * sc;
+            continue;
+        }
+        int64_t q = lo;
+        if (q < hi && (reinterpret_cast<uintptr_t>(vals + q) & 15)) {
+            if (lane == 0) out[q] = vals[q] * sc;
+            ++q;
+        }
+        const int64_t np = (hi - q) >> 1;
+        const double2 *v2 = reinterpret_cast<const double2 *>(vals + q);
+        double2 *o2 = reinterpret_cast<double2 *>(out + q);
+        for (int64_t t = lane; t < np; t += 32) {
+            const double2 x = __ldg(v2 + t);
+            o2[t] = make_double2(x.x * sc, x.y * sc);
+        }
+        if (q + 2 * np < hi && lane == 31) out[hi - 1] = vals[hi - 1] * sc;
     }
 }
 
@@ -341,16 +407,21 @@ __global__ void validate_kernel(const int64_t *indptr, const int32_t *rows, cons
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned f = 0;
     if (tid == 0 && (indptr[0] != 0 || indptr[n] != nnz)) f |= 1;
-    for (int64_t j = tid; j < n; j += nth) {
+    // a warp per column: coalesced row checks, 128-bit value loads
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarps = nth >> 5;
+    for (int64_t j = warp; j < n; j += nwarps) {
         const int64_t lo = indptr[j], hi = indptr[j + 1];
         if (hi < lo) { f |= 2; continue; }
         if (lo < 0 || hi > nnz) { f |= 1; continue; }
-        for (int64_t q = lo; q < hi; ++q) {
+        for (int64_t q = lo + lane; q < hi; q += 32) {
             const int32_t r = rows[q];
             if (r < 0 || r >= R) f |= 4;
-            if (!isfinite(vals[q])) f |= 8;
             if (q > lo && rows[q - 1] >= r) f |= 16;
         }
+        span_f64(vals, lo, hi, lane, 32, [&](int64_t, double x) {
+            if (!isfinite(x)) f |= 8;
+        });
     }
     if (f) atomicOr(flags, f);
 }
