@@ -22,6 +22,16 @@
 //                and red.global.add.f64 scatter of quad*step*a_j into the view.
 //                Concurrent groups read stale views by design (solver.py:8-13,
 //                SPEC.md:261-262); the damping check discards bad epochs.
+//  * scd_seq_narrow / scd_replica — dense columns with d <= 256 (C3): the
+//                view in registers (sequential) or a CTA snapshot plus
+//                per-warp pending updates published per phase (async).
+//
+// Solve variants: chunked solves (stream.cu) guard every kernel with the open
+// chunk's sequence number; GLM_FLAG_TURN solves leave the value check and
+// the finalize to glm_round_turn (peer.cu), which fuses them with the Delta v
+// exchange and the next round's start; GLM_FLAG_PREFETCH_PERM generates the
+// next solve's permutation on a low-priority side stream (early — while this
+// epoch runs — when every solve has exactly one attempt).
 //
 // Memory: delta is double-buffered (every coordinate is visited exactly once
 // per epoch, so the epoch reads delta[dc] and writes delta[dc^1] — accept is a
