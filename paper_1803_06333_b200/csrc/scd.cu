@@ -540,6 +540,118 @@ __global__ void __launch_bounds__(BS) scd_seq(EpochParams p) {
     }
 }
 
+// Deterministic CSC epoch for short columns (<= 32 R entries in registers):
+// one warp, with the permutation entry of k + 3, the column bounds of k + 2
+// and the column + metadata of k + 1 in flight while k is stepped, and the
+// scatter written from the gathered values (no re-load).  Same arithmetic,
+// in the same order, as scd_seq<32>.
+template <int R, bool SMEM>
+__global__ void __launch_bounds__(32) scd_seq_csc(EpochParams p) {
+    SolveState *st = p.st;
+    if (skip_attempt(st, p.seq)) return;
+    extern __shared__ double sview[];
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
+    double *gview = st->vw ? p.view1 : p.view0;
+    double *V = SMEM ? sview : gview;
+    const int lane = threadIdx.x;
+    if (SMEM) {
+        for (int64_t r = lane; r < p.d; r += 32) sview[r] = gview[r];
+        __syncwarp();
+    }
+    struct Col {
+        int j;
+        int64_t lo, hi;
+        int rows[R];
+        double vals[R];
+        double b, dj, s, y;
+    };
+    auto load_col = [&](int j, int64_t lo, int64_t hi, Col &c) {
+        c.j = j;
+        c.lo = lo;
+        c.hi = hi;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t q = lo + lane + 32 * i;
+            const bool in = q < hi;
+            c.rows[i] = in ? __ldg(p.rows + q) : 0;
+            c.vals[i] = in ? __ldg(p.vals + q) : 0.0;
+        }
+        c.b = __ldg(p.base + j);
+        c.dj = dcur ? dcur[j] : 0.0;
+        c.s = __ldg(p.sq + j);
+        c.y = p.y ? __ldg(p.y + j) : 0.0;
+    };
+    const int64_t m = p.m;
+    Col cur;
+    int jA = 0, jB = 0;
+    int64_t loA = 0, hiA = 0;
+    if (m > 0) {
+        const int j0 = __ldg(p.perm);
+        load_col(j0, __ldg(p.indptr + j0), __ldg(p.indptr + j0 + 1), cur);
+    }
+    if (m > 1) {
+        jA = __ldg(p.perm + 1);
+        loA = __ldg(p.indptr + jA);
+        hiA = __ldg(p.indptr + jA + 1);
+    }
+    if (m > 2) jB = __ldg(p.perm + 2);
+    const int kind = p.kind;
+    double gacc = 0.0;
+    for (int64_t k = 0; k < m; ++k) {
+        const Col c = cur;
+        int64_t loB = 0, hiB = 0;
+        int jC = 0;
+        if (k + 1 < m) load_col(jA, loA, hiA, cur);
+        if (k + 2 < m) {
+            loB = __ldg(p.indptr + jB);
+            hiB = __ldg(p.indptr + jB + 1);
+        }
+        if (k + 3 < m) jC = __ldg(p.perm + k + 3);
+        double g[R];
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            g[i] = c.lo + lane + 32 * i < c.hi ? V[c.rows[i]] : 0.0;
+            if (c.lo + lane + 32 * i < c.hi) acc += c.vals[i] * g[i];
+        }
+        for (int64_t q = c.lo + lane + 32 * R; q < c.hi; q += 32) acc += p.vals[q] * V[p.rows[q]];
+        acc = warp_sum(acc);
+        double raw = 0.0;
+        if (!coord_step(kind, p.lam, p.rho, c.y, acc, p.quad * c.s, c.b + c.dj, raw)) {
+            if (lane == 0) flag_error(st);
+            raw = 0.0;
+        }
+        const double step = damping * raw;
+        const double dn = step != 0.0 ? c.dj + step : c.dj;
+        if (lane == 0) {
+            dnext[c.j] = dn;
+            gacc += g_one(kind, p.lam, p.rho, c.y, c.b + dn);
+        }
+        if (step != 0.0) {
+            const double f = p.quad * step;
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (c.lo + lane + 32 * i < c.hi) V[c.rows[i]] = g[i] + f * c.vals[i];
+            for (int64_t q = c.lo + lane + 32 * R; q < c.hi; q += 32) V[p.rows[q]] += f * p.vals[q];
+        }
+        __syncwarp();
+        jA = jB;
+        loA = loB;
+        hiA = hiB;
+        jB = jC;
+    }
+    if (SMEM) {
+        for (int64_t r = lane; r < p.d; r += 32) gview[r] = sview[r];
+    }
+    if (lane == 0) {
+        p.gpart[0] = gacc;
+        st->epoch_blocks = 1;
+    }
+}
+
 // ------------------------------------------------------- value + decide
 // damped_solve's control flow after an attempt (solver.py:272-298; per chunk
 // _train_chunk, pipeline.py:180-193) for the new value G (one thread).
@@ -934,6 +1046,21 @@ constexpr int64_t SMEM_VIEW_MAX = 24 * 1024;   // doubles (192 KB)
 
 template <int BS, bool DENSE>
 static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
+    if (BS == 32 && !DENSE) {   // short CSC columns: the pipelined one-warp kernel
+        if (p.d <= SMEM_VIEW_MAX) {
+            size_t bytes = sizeof(double) * (size_t)(p.d > 0 ? p.d : 1);
+            GLM_CUDA_TRY(cudaFuncSetAttribute(scd_seq_csc<3, true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(SMEM_VIEW_MAX * sizeof(double))));
+            count_launch();
+            scd_seq_csc<3, true><<<1, 32, bytes, s>>>(p);
+        } else {
+            count_launch();
+            scd_seq_csc<3, false><<<1, 32, 0, s>>>(p);
+        }
+        GLM_CUDA_TRY(cudaGetLastError());
+        return GLM_OK;
+    }
     if (p.d <= SMEM_VIEW_MAX) {
         size_t bytes = sizeof(double) * (size_t)(p.d > 0 ? p.d : 1);
         GLM_CUDA_TRY(cudaFuncSetAttribute(scd_seq<BS, true, DENSE>,
