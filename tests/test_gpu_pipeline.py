@@ -200,3 +200,21 @@ def test_empty_and_single_chunk_edges():
                                                         seed=0, epoch_index=0, epochs=2)
         assert st == 0 and len(values) == 2 and values[1] <= values[0] <= scal[0]
         part.close()
+
+
+@pytest.mark.parametrize("kind,k", [("ridge_primal", 2), ("lasso_primal", 3)])
+def test_chunked_primal_kinds_vs_oracle(kind, k):
+    """Primal kinds stream feature columns (the GLMCHUNK row vector is the
+    target b, cli.py:182-185): streamed chunked epochs vs the oracle's."""
+    rng = np.random.default_rng(17)
+    m = _synth(3_000, 4_000, 20, 17, labels=False)          # columns = features
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    b = rng.standard_normal(m.n_rows)
+    spec = g.ObjectiveSpec(kind, 0.5, m.n_rows, m.n_cols, target=b)
+    part = P.StreamingPartition(m, chunk_size=700, device_budget=1)
+    runner = P.chunked_device_runner(part, seed=6, epochs=2)
+    res = _train(m, spec, runner, 3, 2, 6)
+    want = oracle.train_chunked(om, k, 0.5, 700, target=b, epochs=2, seed=6, rounds=3)
+    np.testing.assert_allclose(res.trace.objectives(), want["objective"], rtol=1e-10)
+    np.testing.assert_allclose(res.model.alpha, want["alpha"], atol=1e-8)
+    part.close()
