@@ -139,6 +139,10 @@ int glm_version(void);
 /* Number of kernels this library has launched (process-wide, monotone). */
 long long glm_launch_count(void);
 int glm_device_count(int *out);
+/* Debug: kernels record min start / max end %globaltimer (ns) into device
+ * u64[16] slot pairs: [0,1] epoch, [2,3] first permutation kernel, [4,5] last
+ * permutation kernel, [6,7] round turn.  NULL: off. */
+int glm_debug_timeline(unsigned long long *device_slots);
 /* Host-side xorshift64 jump: state after `steps` steps (solver.py:41-46). */
 uint64_t glm_xorshift_jump(uint64_t state, uint64_t steps);
 uint64_t glm_derive_seed(uint64_t base, const uint64_t *idx, int n_idx); /* solver.py:57-61 */

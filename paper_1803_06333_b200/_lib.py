@@ -70,6 +70,7 @@ SIGNATURES = {
     "glm_solver_timing_peek": (ctypes.c_int, [_P, _P, _P]),
     "glm_solver_timing_glue": (ctypes.c_int, [_P, _P, _P, ctypes.c_int]),
     "glm_device_count": (ctypes.c_int, [_P]),
+    "glm_debug_timeline": (ctypes.c_int, [_P]),
     "glm_xorshift_jump": (_c_u64, [_c_u64, _c_u64]),
     "glm_derive_seed": (_c_u64, [_c_u64, _P, ctypes.c_int]),
     "glm_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_i64, _c_i64, _P, _P, _P, _P]),

@@ -117,6 +117,14 @@ int glm_solver_timing_glue(glm_solver *s, double *ms_out, int32_t *n_out, int co
     return GLM_OK;
 }
 
+// Debug timeline: kernels write earliest start / latest end %globaltimer
+// stamps into device u64[2 * TL_SLOTS] (epoch, first and last permutation
+// kernel, round turn); NULL turns it off.
+int glm_debug_timeline(unsigned long long *device_slots) {
+    GLM_CUDA_TRY(cudaMemcpyToSymbol(d_timeline, &device_slots, sizeof(device_slots)));
+    return GLM_OK;
+}
+
 int glm_device_count(int *out) {
     GLM_CUDA_TRY(cudaGetDeviceCount(out));
     return GLM_OK;

@@ -258,6 +258,28 @@ __device__ __forceinline__ double f_conj_term(int kind, double lam, double tgt, 
 // Host-side count of kernels this library launched (bench.py "gpu_launches").
 void count_launch();
 
+// Debug timeline (glm_debug_timeline): when set, kernels record the earliest
+// start (atomicMin) and latest end (atomicMax) of %globaltimer in slot pairs.
+enum { TL_EPOCH = 0, TL_PERM_FIRST = 1, TL_PERM_LAST = 2, TL_TURN = 3, TL_SLOTS = 8 };
+__device__ unsigned long long *d_timeline = nullptr;   // (one translation unit)
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_start(int slot) {
+    unsigned long long *t = d_timeline;
+    if (t && threadIdx.x == 0) atomicMin(t + 2 * slot, tl_now());
+}
+__device__ __forceinline__ void tl_end(int slot) {
+    unsigned long long *t = d_timeline;
+    if (t && threadIdx.x == 0) atomicMax(t + 2 * slot + 1, tl_now());
+}
+__device__ __forceinline__ void tl_end_warp(int slot) {
+    unsigned long long *t = d_timeline;
+    if (t && (threadIdx.x & 31) == 0) atomicMax(t + 2 * slot + 1, tl_now());
+}
+
 }  // namespace glm
 
 #define GLM_CUDA_TRY(expr)                                                   \

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     __shared__ int s_dc, s_vw;
     SolveState *st = p.st;
     volatile SolveState *vst = st;
+    tl_start(TL_TURN);
     if (threadIdx.x == 0) {
         s_turn0 = vst->turn;
         s_R = p.ctl[0];
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         p.view1[r] = g;
     }
     if (!reduce_last<1>(acc, p.scratch)) return;
+    tl_end(TL_TURN);
     double f = acc[0];
     if (dual) f = f / (2.0 * p.lam);
     else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;

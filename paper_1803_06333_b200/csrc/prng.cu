@@ -194,7 +194,10 @@ template <class Src>
 __global__ void __launch_bounds__(PERM_THREADS) hist_kernel(Src src, int64_t n, int shift,
                                                             uint32_t *hist) {
     if (src.skip()) return;
+    tl_start(TL_PERM_FIRST);
     for_keys(src, n, [&](int64_t, uint32_t k) { atomicAdd(hist + (k >> shift), 1u); });
+    __syncthreads();
+    tl_end(TL_PERM_FIRST);
 }
 
 template <class Src>
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(BS_WARPS * 32) bucket_sort_kernel(const SolveS
                                                                     const uint32_t *offs,
                                                                     int64_t nbk, int32_t *perm) {
     if (st && st->done) return;
+    tl_start(TL_PERM_LAST);
     __shared__ uint64_t sbuf[BS_WARPS][BS_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = ((int64_t)blockIdx.x * BS_WARPS + warp) * 32;
@@ -330,10 +334,12 @@ __global__ void __launch_bounds__(BS_WARPS * 32) bucket_sort_kernel(const SolveS
         insertion_sort(buf + (my_lo - lo), (int)(my_hi - my_lo));
         __syncwarp();
         for (uint32_t i = lane; i < n; i += 32) perm[lo + i] = (int32_t)(uint32_t)buf[i];
+        tl_end_warp(TL_PERM_LAST);
     } else {                     // rare: sort in place in global memory
         insertion_sort(pairs + my_lo, (int)(my_hi - my_lo));
         __syncwarp();
         for (uint32_t i = lane; i < n; i += 32) perm[lo + i] = (int32_t)(uint32_t)pairs[lo + i];
+        tl_end_warp(TL_PERM_LAST);
     }
 }
 

@@ -113,6 +113,7 @@ template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
     if (skip_attempt(st, p.seq)) return;
+    tl_start(TL_EPOCH);
     // CM bit 0: gather the view through L1 (ld.ca); bit 1: stream the column
     // with L1::no_allocate + L2 evict_first, view traffic evict_last.
     const uint64_t pol_col = (CM & 2) ? policy_evict_first() : 0;
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
         }
     }
     store_block_gsum(gacc, p.gpart, st);
+    tl_end(TL_EPOCH);
 }
 
 
