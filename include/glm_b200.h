@@ -215,6 +215,15 @@ size_t glm_argsort_temp_bytes(int64_t n);
 /* stable argsort of u32 keys -> int32 perm (np.argsort(kind="stable")) */
 int glm_argsort_u32(const uint32_t *keys, int64_t n, int32_t *perm, void *temp,
                     size_t temp_bytes, void *stream);
+/* Fused generate + stable argsort, the solver's own permutation path:
+ * PermutationGenerator(state).permute(n) (solver.py:86-89) and
+ * keys_to_permutation(generate_keys(seed, n)) (pipeline.py:29-78).  The keys
+ * are regenerated in both passes, never stored.  temp: glm_argsort_temp_bytes(n)
+ * bytes, zeroed by the call. */
+int glm_perm(uint64_t state, int64_t n, int32_t *perm, void *temp, size_t temp_bytes,
+             void *stream);
+int glm_chunk_perm(uint64_t seed, int64_t n, int32_t *perm, void *temp, size_t temp_bytes,
+                   void *stream);
 
 /* Data layer (data.py:98-187, cli.py:146-185).  All device pointers. */
 int glm_col_sqnorms(const glm_matrix *A, double *out, void *stream);

@@ -89,6 +89,8 @@ SIGNATURES = {
     "glm_chunk_keys": (ctypes.c_int, [_c_u64, _c_i64, _P, _P]),
     "glm_argsort_temp_bytes": (ctypes.c_size_t, [_c_i64]),
     "glm_argsort_u32": (ctypes.c_int, [_P, _c_i64, _P, _P, ctypes.c_size_t, _P]),
+    "glm_perm": (ctypes.c_int, [_c_u64, _c_i64, _P, _P, ctypes.c_size_t, _P]),
+    "glm_chunk_perm": (ctypes.c_int, [_c_u64, _c_i64, _P, _P, ctypes.c_size_t, _P]),
     "glm_col_sqnorms": (ctypes.c_int, [_P, _P, _P]),
     "glm_matvec": (ctypes.c_int, [_P, _P, _P, _P]),
     "glm_rmatvec": (ctypes.c_int, [_P, _P, _P, _P]),

@@ -260,7 +260,8 @@ void count_launch();
 
 // Debug timeline (glm_debug_timeline): when set, kernels record the earliest
 // start (atomicMin) and latest end (atomicMax) of %globaltimer in slot pairs.
-enum { TL_EPOCH = 0, TL_PERM_FIRST = 1, TL_PERM_LAST = 2, TL_TURN = 3, TL_SLOTS = 8 };
+enum { TL_EPOCH = 0, TL_PERM_FIRST = 1, TL_PERM_LAST = 2, TL_TURN = 3, TL_SCAN = 4, TL_SCATTER = 5,
+       TL_SLOTS = 8 };
 __device__ unsigned long long *d_timeline = nullptr;   // (one translation unit)
 __device__ __forceinline__ unsigned long long tl_now() {
     unsigned long long t;

@@ -15,14 +15,21 @@
 // chunk stream the 4096-key CUDA block *is* the reference's key block, so the
 // base state is derive_seed(seed, block).
 //
-// The stable argsort never materialises the keys: pass 1 histograms the top
-// `nb` key bits (nb chosen for ~8 keys per bucket), a two-kernel parallel
-// scan turns the histogram into bucket offsets, pass 2 regenerates the keys
-// and scatters (key<<32 | index) into the buckets, and a warp per 32 buckets
-// stages its ~256 pairs in shared memory, insertion-sorts each bucket by
-// (key, index) — exactly numpy's stable order — and writes the permutation
-// coalesced.  Oversized bucket groups fall back to an in-place sort in global
-// memory (slower, same result).
+// The stable argsort never materialises the keys.  Two variants, same order:
+//  * row counts (generated keys, n <= 2^21 — every partition and chunk of the
+//    configs): pass 1 histograms each 4096-key block's top `nb2` bits (~512
+//    keys per bucket) in shared memory, writes one count row per block and
+//    saves every thread's start state; a column scan turns the rows into
+//    per-(block, bucket) offsets; pass 2 re-walks the keys from the saved
+//    states and scatters (key<<32 | index) through shared-memory cursors; one
+//    CTA per bucket spreads its pairs over 256 sub-buckets (the next 8 key
+//    bits) in shared memory and each thread insertion-sorts one sub-bucket.
+//    No global atomics; 4 kernels.
+//  * global buckets (larger n, and argsort of caller keys): pass 1 histograms
+//    the top `nb` bits (~8 keys per bucket) with global atomics, a two-kernel
+//    scan gives bucket offsets, pass 2 regenerates the keys and scatters, and
+//    a warp per 32 buckets insertion-sorts them in shared memory.  Oversized
+//    bucket groups fall back to an in-place sort in global memory.
 #include <algorithm>
 #include <mutex>
 
@@ -36,7 +43,7 @@ constexpr int KPT = 16;                             // keys per thread
 constexpr int KEYS_PER_BLOCK = PERM_THREADS * KPT;  // 4096 == pipeline.KEY_BLOCK
 
 __device__ uint64_t d_jump_cols[64 * 64];            // [i][b]: column b of M^(2^i)
-__device__ uint64_t d_thread_jump[PERM_THREADS * 64];  // [t][b]: column b of M^(16 t)
+__device__ uint64_t d_thread_jump[PERM_THREADS * 64];  // [b][t]: column b of M^(16 t)
 
 static uint64_t h_jump_cols[64 * 64];
 static uint64_t h_thread_jump[PERM_THREADS * 64];
@@ -68,7 +75,7 @@ static void build_host_jump() {
     for (int b = 0; b < 64; ++b) {
         uint64_t s = 1ULL << b;
         for (int t = 0; t < PERM_THREADS; ++t) {
-            h_thread_jump[t * 64 + b] = s;
+            h_thread_jump[b * PERM_THREADS + t] = s;   // [b][t]: a warp's loads coalesce
             for (int k = 0; k < KPT; ++k) s = xs_step(s);
         }
     }
@@ -107,24 +114,36 @@ __device__ __forceinline__ uint64_t xor_reduce_warp(uint64_t v) {
     return v;
 }
 
-// Warp-cooperative jump: all 32 lanes call with the same (state, steps).
+// Warp-cooperative jump: all 32 lanes call with the same (state, steps).  The
+// matrix columns do not depend on the state, so the next set bit's columns are
+// loaded while the current product is XOR-reduced.
 __device__ __forceinline__ uint64_t warp_jump(uint64_t state, uint64_t steps) {
     const int lane = threadIdx.x & 31;
-    for (int i = 0; steps; ++i, steps >>= 1) {
-        if (!(steps & 1)) continue;
-        const uint64_t *c = d_jump_cols + i * 64;
-        uint64_t part = (((state >> lane) & 1) ? c[lane] : 0ULL) ^
-                        (((state >> (lane + 32)) & 1) ? c[lane + 32] : 0ULL);
+    if (!steps) return state;
+    int i = __ffsll((long long)steps) - 1;
+    uint64_t c0 = d_jump_cols[i * 64 + lane], c1 = d_jump_cols[i * 64 + lane + 32];
+    for (;;) {
+        steps &= steps - 1;
+        const int nx = steps ? __ffsll((long long)steps) - 1 : -1;
+        uint64_t n0 = 0, n1 = 0;
+        if (nx >= 0) {
+            n0 = d_jump_cols[nx * 64 + lane];
+            n1 = d_jump_cols[nx * 64 + lane + 32];
+        }
+        const uint64_t part = (((state >> lane) & 1) ? c0 : 0ULL) ^
+                              (((state >> (lane + 32)) & 1) ? c1 : 0ULL);
         state = xor_reduce_warp(part);
+        if (nx < 0) return state;
+        c0 = n0;
+        c1 = n1;
     }
-    return state;
 }
 
 __device__ __forceinline__ uint64_t thread_apply(uint64_t state) {
-    const uint64_t *c = d_thread_jump + threadIdx.x * 64;
+    const uint64_t *c = d_thread_jump + threadIdx.x;
     uint64_t y = 0;
-#pragma unroll 16
-    for (int b = 0; b < 64; ++b) y ^= ((state >> b) & 1) ? __ldg(c + b) : 0ULL;
+#pragma unroll
+    for (int b = 0; b < 64; ++b) y ^= ((state >> b) & 1) ? __ldg(c + b * PERM_THREADS) : 0ULL;
     return y;
 }
 
@@ -164,9 +183,24 @@ struct ChunkKeys {        // generate_keys(seed, n)
     }
 };
 
-// Runs f(q, key) over this thread's KPT keys.
+// Thread's KPT keys from its start state s.
+template <class F>
+__device__ __forceinline__ void walk_keys(uint64_t s, int64_t n, F f) {
+    const int64_t q0 = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (int64_t)threadIdx.x * KPT;
+    if (q0 >= n) return;
+    const int cnt = (int)(n - q0 < KPT ? n - q0 : KPT);
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+        s = dev_xs(s);
+        if (i < cnt) f(q0 + i, (uint32_t)s);
+    }
+}
+
+// Runs f(q, key) over this thread's KPT keys; saves the thread's start state
+// to tstate[global thread] when given (a second pass reads it back).
 template <class Src, class F>
-__device__ __forceinline__ void for_keys(const Src &src, int64_t n, F f) {
+__device__ __forceinline__ void for_keys(const Src &src, int64_t n, F f,
+                                         uint64_t *tstate = nullptr) {
     __shared__ uint64_t s_base;
     if (threadIdx.x < 32) {
         const uint64_t b = src.block_base();
@@ -175,13 +209,9 @@ __device__ __forceinline__ void for_keys(const Src &src, int64_t n, F f) {
     __syncthreads();
     const int64_t q0 = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (int64_t)threadIdx.x * KPT;
     if (q0 >= n) return;
-    uint64_t s = thread_apply(s_base);
-    const int cnt = (int)(n - q0 < KPT ? n - q0 : KPT);
-#pragma unroll
-    for (int i = 0; i < KPT; ++i) {
-        s = dev_xs(s);
-        if (i < cnt) f(q0 + i, (uint32_t)s);
-    }
+    const uint64_t s = thread_apply(s_base);
+    if (tstate) tstate[(size_t)blockIdx.x * PERM_THREADS + threadIdx.x] = s;
+    walk_keys(s, n, f);
 }
 
 template <class Src>
@@ -343,6 +373,226 @@ __global__ void __launch_bounds__(BS_WARPS * 32) bucket_sort_kernel(const SolveS
     }
 }
 
+// ------------------------------------------------- row-count variant (v2)
+constexpr int V2_MAX_LOG = 21;
+constexpr int BS2_THREADS = 256;
+constexpr int BS2_CAP = 1024;          // pairs per bucket sorted in shared memory
+constexpr int CS_WARPS = 32;
+
+__device__ __forceinline__ uint32_t bucket_of(uint32_t k, int nb) {
+    return nb ? k >> (32 - nb) : 0u;
+}
+
+template <class Src>
+__global__ void __launch_bounds__(PERM_THREADS) hist2_kernel(Src src, int64_t n, int nb,
+                                                             uint32_t *counts, uint64_t *tstate) {
+    if (src.skip()) return;
+    tl_start(TL_PERM_FIRST);
+    extern __shared__ uint32_t h2[];
+    const int NB = 1 << nb;
+    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) h2[i] = 0;
+    __syncthreads();
+    for_keys(src, n, [&](int64_t, uint32_t k) { atomicAdd(h2 + bucket_of(k, nb), 1u); }, tstate);
+    __syncthreads();
+    uint32_t *row = counts + (size_t)blockIdx.x * NB;
+    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) row[i] = h2[i];
+    tl_end(TL_PERM_FIRST);
+}
+
+// Grid NB/32 CTAs of 32 warps; lane = bucket, warp = a contiguous segment of
+// the count rows.  Rows become exclusive offsets within the bucket; tot[b] =
+// bucket total; the last CTA writes boff = exclusive scan of tot.
+__global__ void __launch_bounds__(CS_WARPS * 32) colscan2_kernel(const SolveState *st,
+                                                                 uint32_t *counts, int nblk,
+                                                                 int nb, uint32_t *tot,
+                                                                 uint32_t *boff,
+                                                                 uint32_t *ticket) {
+    if (st && st->done) return;
+    tl_start(TL_SCAN);
+    __shared__ uint32_t s_part[CS_WARPS][32];
+    __shared__ uint32_t s_warp[CS_WARPS];
+    __shared__ bool s_last;
+    const int NB = 1 << nb;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.x * 32 + lane;
+    const int r0 = (int)((int64_t)nblk * w / CS_WARPS);
+    const int r1 = (int)((int64_t)nblk * (w + 1) / CS_WARPS);
+    uint32_t sum = 0;
+    if (b < NB) {
+        for (int r = r0; r < r1; r += 8) {
+            uint32_t c[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) c[j] = r + j < r1 ? counts[(size_t)(r + j) * NB + b] : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += c[j];
+        }
+    }
+    s_part[w][lane] = sum;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < CS_WARPS; ++j) {
+            const uint32_t x = s_part[j][lane];
+            s_part[j][lane] = acc;
+            acc += x;
+        }
+        if (b < NB) tot[b] = acc;
+    }
+    __syncthreads();
+    if (b < NB) {
+        uint32_t run = s_part[w][lane];
+        for (int r = r0; r < r1; r += 8) {
+            uint32_t c[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) c[j] = r + j < r1 ? counts[(size_t)(r + j) * NB + b] : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (r + j < r1) {
+                    counts[(size_t)(r + j) * NB + b] = run;
+                    run += c[j];
+                }
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    tl_end(TL_SCAN);
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // exclusive scan of the NB (<= 4096) totals: `per` (<= 4) consecutive per thread
+    const int per = (NB + CS_WARPS * 32 - 1) / (CS_WARPS * 32);
+    const int i0 = threadIdx.x * per;
+    uint32_t v[4];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[j] = j < per && i0 + j < NB ? __ldcg(tot + i0 + j) : 0u;
+        mine += v[j];
+    }
+    uint32_t inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    uint32_t pre = inc - mine;
+    for (int j = 0; j < w; ++j) pre += s_warp[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < per && i0 + j < NB) {
+            boff[i0 + j] = pre;
+            pre += v[j];
+        }
+    if (threadIdx.x == CS_WARPS * 32 - 1) {
+        boff[NB] = pre;
+        *ticket = 0;              // ready for the next permutation
+    }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(PERM_THREADS) scatter2_kernel(Src src, int64_t n, int nb,
+                                                                const uint32_t *counts,
+                                                                const uint32_t *boff,
+                                                                const uint64_t *tstate,
+                                                                uint64_t *pairs) {
+    if (src.skip()) return;
+    tl_start(TL_SCATTER);
+    extern __shared__ uint32_t cur2[];
+    const int NB = 1 << nb;
+    const uint32_t *row = counts + (size_t)blockIdx.x * NB;
+    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) cur2[i] = boff[i] + row[i];
+    __syncthreads();
+    walk_keys(tstate[(size_t)blockIdx.x * PERM_THREADS + threadIdx.x], n,
+              [&](int64_t q, uint32_t k) {
+        const uint32_t pos = atomicAdd(cur2 + bucket_of(k, nb), 1u);
+        pairs[pos] = ((uint64_t)k << 32) | (uint32_t)q;
+    });
+    __syncthreads();
+    tl_end(TL_SCATTER);
+}
+
+// One CTA per bucket (~512 pairs): a counting pass on the next 8 key bits
+// spreads the pairs over 256 sub-buckets in shared memory (~2 pairs each),
+// then thread t insertion-sorts sub-bucket t by (key, index) — numpy's stable
+// order — and the CTA writes its slice of the permutation coalesced.
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_warp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    uint32_t pre = inc - x;
+    for (int j = 0; j < w; ++j) pre += s_warp[j];
+    return pre;
+}
+
+__global__ void __launch_bounds__(BS2_THREADS) bsort2_kernel(const SolveState *st,
+                                                             uint64_t *pairs,
+                                                             const uint32_t *boff, int nb,
+                                                             int32_t *perm) {
+    if (st && st->done) return;
+    tl_start(TL_PERM_LAST);
+    __shared__ uint64_t s_in[BS2_CAP], s_out[BS2_CAP];
+    __shared__ uint32_t s_cur[BS2_THREADS];
+    __shared__ uint32_t s_warp[BS2_THREADS / 32];
+    const uint32_t lo = boff[blockIdx.x], hi = boff[blockIdx.x + 1];
+    const int cnt = (int)(hi - lo);
+    const int t = threadIdx.x;
+    if (cnt <= BS2_CAP) {
+        const int sh = 24 - nb;                    // the 8 key bits below the bucket bits
+        s_cur[t] = 0;
+        __syncthreads();
+        for (int i = t; i < cnt; i += BS2_THREADS) {
+            const uint64_t p = pairs[lo + i];
+            s_in[i] = p;
+            atomicAdd(s_cur + ((uint32_t)(p >> 32) >> sh & 255u), 1u);
+        }
+        __syncthreads();
+        const uint32_t c = s_cur[t];
+        const uint32_t ex = block_excl_scan_256(c, s_warp);
+        s_cur[t] = ex;
+        __syncthreads();
+        for (int i = t; i < cnt; i += BS2_THREADS) {
+            const uint64_t p = s_in[i];
+            s_out[atomicAdd(s_cur + ((uint32_t)(p >> 32) >> sh & 255u), 1u)] = p;
+        }
+        __syncthreads();
+        insertion_sort(s_out + ex, (int)c);
+        __syncthreads();
+        for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)s_out[i];
+    } else {                      // never seen with uniform keys; same order, slowly
+        if (t == 0) insertion_sort(pairs + lo, cnt);
+        __syncthreads();
+        for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)pairs[lo + i];
+    }
+    tl_end(TL_PERM_LAST);
+}
+
+static int v2_bits(int64_t n) {       // ~512 keys per bucket, <= 4096 buckets
+    int lg = 0;
+    while ((1LL << lg) < n) ++lg;
+    int nb = lg - 9;
+    if (nb < 0) nb = 0;
+    if (nb > 12) nb = 12;
+    return nb;
+}
+
+static size_t v2_bytes(int64_t capacity) {
+    const int64_t c = std::min<int64_t>(capacity > 0 ? capacity : 1, 1LL << V2_MAX_LOG);
+    const int64_t nblk = (c + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
+    const int64_t NB = 1LL << v2_bits(c);
+    return sizeof(uint32_t) * (size_t)(nblk * NB + 2 * NB + 2 + 64) +
+           sizeof(uint64_t) * (size_t)(nblk * PERM_THREADS) + 256;
+}
+
 // ---------------------------------------------------------------------------
 int bucket_bits(int64_t n) {
     int lg = 0;
@@ -357,7 +607,7 @@ size_t perm_scratch_bytes(int64_t n) {
     const int64_t nbk = 1LL << bucket_bits(n);
     const size_t a = sizeof(uint64_t) * (size_t)(n > 0 ? n : 1);             // pairs
     const size_t h = sizeof(uint32_t) * (size_t)(3 * nbk + 1 + nbk / SCAN_TILE + 2);
-    return a + h + 1024;
+    return a + h + 1024 + v2_bytes(n) + 256;
 }
 
 PermScratch carve_perm_scratch(void *base, int64_t capacity, int64_t n) {
@@ -375,6 +625,19 @@ PermScratch carve_perm_scratch(void *base, int64_t capacity, int64_t n) {
     p.offs = p.hist + nbk_cap;
     p.cursor = p.offs + nbk_cap + 1;
     p.flags = p.cursor + nbk_cap;     // tile sums (nbk_cap / SCAN_TILE + 1)
+    c = (char *)(p.flags + nbk_cap / SCAN_TILE + 2);
+    c = (char *)(((uintptr_t)c + 255) & ~(uintptr_t)255);
+    p.ticket = (uint32_t *)c;         // zero between uses (the last scan CTA resets it)
+    p.v2 = n <= (1LL << V2_MAX_LOG) && capacity > 0;
+    p.nb2 = v2_bits(n);
+    const int64_t c2 = std::min<int64_t>(capacity > 0 ? capacity : 1, 1LL << V2_MAX_LOG);
+    const int64_t nb2_cap = 1LL << v2_bits(c2);
+    p.tot = p.ticket + 64;
+    p.boff = p.tot + nb2_cap;
+    p.counts = p.boff + nb2_cap + 1;
+    const int64_t nblk_cap = (c2 + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
+    c = (char *)(p.counts + nblk_cap * nb2_cap);
+    p.tstate = (uint64_t *)(((uintptr_t)c + 255) & ~(uintptr_t)255);
     return p;
 }
 
@@ -385,6 +648,23 @@ static int perm_from_source(const Src &src, const SolveState *st, int64_t n, int
                             const PermScratch &sc, cudaStream_t stream,
                             const uint32_t *keys_array) {
     if (n <= 0) return GLM_OK;
+    if (!keys_array && sc.v2) {
+        const int NB = 1 << sc.nb2;
+        const int nblk = key_blocks(n);
+        const size_t hsm = sizeof(uint32_t) * (size_t)NB;
+        count_launch();
+        hist2_kernel<<<nblk, PERM_THREADS, hsm, stream>>>(src, n, sc.nb2, sc.counts, sc.tstate);
+        count_launch();
+        colscan2_kernel<<<(NB + 31) / 32, CS_WARPS * 32, 0, stream>>>(
+            st, sc.counts, nblk, sc.nb2, sc.tot, sc.boff, sc.ticket);
+        count_launch();
+        scatter2_kernel<<<nblk, PERM_THREADS, hsm, stream>>>(src, n, sc.nb2, sc.counts, sc.boff,
+                                                            sc.tstate, sc.pairs);
+        count_launch();
+        bsort2_kernel<<<NB, BS2_THREADS, 0, stream>>>(st, sc.pairs, sc.boff, sc.nb2, perm);
+        GLM_CUDA_TRY(cudaGetLastError());
+        return GLM_OK;
+    }
     const int shift = 32 - sc.nb;
     const int tiles = (int)((sc.nbk + SCAN_TILE - 1) / SCAN_TILE);
     const int agrid = (int)std::min<int64_t>((n + 255) / 256, NUM_SMS * 16);

@@ -14,6 +14,11 @@ struct PermScratch {
     uint32_t *offs = nullptr;    // nbk + 1
     uint32_t *cursor = nullptr;
     uint32_t *flags = nullptr;   // [0] max bucket size
+    // row-count variant (generated keys, n <= 2^21)
+    bool v2 = false;
+    int nb2 = 0;
+    uint32_t *ticket = nullptr, *tot = nullptr, *boff = nullptr, *counts = nullptr;
+    uint64_t *tstate = nullptr;  // per-thread key-stream start states (pass 1 -> pass 2)
 };
 
 uint64_t host_jump(uint64_t state, uint64_t steps);

@@ -1318,7 +1318,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         if (!(launched == 0 && have_perm0))
             r = stream_perm(s->st, 0, (uint64_t)launched * (uint64_t)m, m, P, ps, stream);
         if (r) return r;
-        if (early && launched == 0) {
+        auto fork = [&]() -> int {
             if ((r = ensure_side())) return r;
             GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
             GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
@@ -1327,7 +1327,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             s->prefetched = true;
             s->prefetch_m = m;
             s->prefetch_alt = true;
-        }
+            return GLM_OK;
+        };
+        if (early && launched == 0 && (r = fork())) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[1], stream));
         if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
             count_launch();

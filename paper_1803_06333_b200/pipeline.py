@@ -47,6 +47,16 @@ def generate_keys(seed, n, n_threads=1):
     return _D().to_host(generate_keys_device(seed, n)).astype(np.uint32)
 
 
+def chunk_permutation(seed, n):
+    """keys_to_permutation(generate_keys(seed, n)) fused on the GPU (the
+    streaming solver's own path, glm_chunk_perm)."""
+    from .solver import _fused_perm
+    if n <= 0:
+        return np.empty(0, dtype=np.int64)
+    return _D().to_host(_fused_perm(L.lib().glm_chunk_perm, seed, n,
+                                    "glm_chunk_perm")).astype(np.int64)
+
+
 def keys_to_permutation(keys):
     """Stable argsort of the keys (pipeline.py:76-78), on the GPU."""
     from .solver import argsort_u32_device

@@ -96,17 +96,28 @@ class PermutationGenerator:
         return _D().to_host(self.keys_device(n)).astype(np.uint32)
 
     def permute_device(self, n):
-        """Stable argsort of the next n keys (int32, on device)."""
+        """Stable argsort of the next n keys (int32, on device): the solver's
+        fused path (glm_perm, keys regenerated, never stored)."""
         D = _D()
         if n <= 0:
             return torch.empty(0, dtype=torch.int32, device=D.device())
-        keys = self.keys_device(n)
-        return argsort_u32_device(keys)
+        perm = _fused_perm(L.lib().glm_perm, self.state, n, "glm_perm")
+        self.advance(n)
+        return perm
 
     def permute(self, n):
         if n <= 0:
             return np.empty(0, dtype=np.int64)
         return _D().to_host(self.permute_device(n)).astype(np.int64)
+
+
+def _fused_perm(fn, seed, n, name):
+    D = _D()
+    perm = torch.empty(n, dtype=torch.int32, device=D.device())
+    nb = L.lib().glm_argsort_temp_bytes(n)
+    tmp = torch.empty(nb, dtype=torch.uint8, device=D.device())
+    L.check(fn(int(seed) & ((1 << 64) - 1), n, D.ptr(perm), D.ptr(tmp), nb, D.sptr()), name)
+    return perm
 
 
 def argsort_u32_device(keys):

@@ -47,7 +47,9 @@ def test_permutation_stream_bit_exact(golden):
 
 
 def test_permutation_large_vs_oracle():
-    for seed, n in [(5, 1), (7, 4095), (11, 131_073), (13, 1_000_003)]:
+    # row-count argsort up to 2^21 keys, global-bucket argsort above
+    for seed, n in [(5, 1), (6, 2), (7, 4095), (11, 131_073), (13, 1_000_003), (17, 1 << 21),
+                    (19, (1 << 21) + 1)]:
         gen = g.PermutationGenerator(seed)
         got = gen.permute(n)
         want, st = oracle.permute(seed, n)
@@ -64,6 +66,9 @@ def test_chunk_keys_bit_exact(golden):
                                       z[f"gk{c}_perm"])
     big = pipeline.generate_keys(99, 300_001)
     np.testing.assert_array_equal(big, oracle.generate_keys(99, 300_001))
+    for seed, n in [(3, 1), (4, 600), (99, 300_001), (7, 1 << 21), (8, 3_000_017)]:
+        np.testing.assert_array_equal(pipeline.chunk_permutation(seed, n),
+                                      oracle.argsort_stable(oracle.generate_keys(seed, n)))
 
 
 def test_argsort_adversarial_ties():

@@ -30,10 +30,11 @@ for r in range(40):
     torch.cuda.synchronize()
     s = slots.cpu().numpy().astype(np.float64)
     t0 = s[0]
-    rows_.append([(s[i] - t0) / 1e3 if s[i] not in (0, 2**63 - 1) else np.nan for i in range(8)])
+    rows_.append([(s[i] - t0) / 1e3 if s[i] not in (0, 2**63 - 1) else np.nan for i in range(12)])
 L.lib().glm_debug_timeline(None)
 med = np.nanmedian(np.array(rows_[5:]), axis=0)
 names = ["epoch start", "epoch end", "perm first start", "perm first end", "perm last start",
-         "perm last end", "turn start", "turn end"]
+         "perm last end", "turn start", "turn end", "perm scan start", "perm scan end",
+         "perm scatter start", "perm scatter end"]
 for n, v in zip(names, med):
     print(f"{n:18s} {v:9.2f} us")
