@@ -7,8 +7,10 @@
 // model (engine.py:271-272, 242-250, 148-166) and solve start (solver.py:
 // 268-270).  Here:
 //
-//   finalize (rank r):  alpha += delta; dv_r[b] = B delta; publish  flag_r = R+1
-//   round start:        wait flag_j >= R for all j (acquire, system scope);
+//   finalize (rank r):  alpha += delta; dv_r[b] = B delta; publish: flag slot r
+//                       of every rank = R+1 (release, system scope, NVLink store)
+//   round start:        wait until every LOCAL flag slot j >= R (acquire,
+//                       system scope; no remote round trip per poll);
 //                       v += sum_j dv_j[b] in ascending rank order (the bits of
 //                       canonical_sum on every rank); grad = f'(v); lin = grad;
 //                       view = lin; f(v); solver state reset (begin)
@@ -26,11 +28,14 @@
 struct glm_peer {
     int device = 0, rank = 0, world = 1;
     int64_t d = 0;
-    char *mem = nullptr;          // [ctl: 8 x i64 | pad to 256 B | dv: 2 x d doubles]
-    int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter
+    // [ctl: 8 x i64 | flag slots: world x i64 | pad to 256 B | dv: 2 x d doubles]
+    char *mem = nullptr;
+    int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter,
+                                  // [3] "every rank published" (turn)
+    int64_t *flags = nullptr;     // local slots: flags[j] = last round rank j published
     double *dv = nullptr;
     double **bufs_dev = nullptr;  // world pointers to each rank's dv (device array)
-    int64_t **flags_dev = nullptr;
+    int64_t **flags_dev = nullptr;  // world pointers to each rank's flag slots
     std::vector<void *> opened;   // cudaIpc-opened peer allocations
     uint64_t *stamps = nullptr;   // glm_peer_stamps: turn phase timestamps (debug)
     cudaIpcMemHandle_t handle{};
@@ -40,6 +45,7 @@ namespace glm {
 
 constexpr int PEER_BLOCKS = 2 * NUM_SMS;
 constexpr int PEER_THREADS = 256;
+constexpr int PEER_MAX_WORLD = 24;      // flag slots that fit the 256-byte header
 
 __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
     int64_t v;
@@ -51,13 +57,48 @@ __device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
     asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Strong store without its own fence: after one fence.sc.sys, a run of these
+// forms the release pattern for each (one MEMBAR.SYS instead of one per store).
+__device__ __forceinline__ void st_relaxed_sys(int64_t *p, int64_t v) {
+    asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Publish round R (one thread, after every block's writes were fenced): our
+// slot in every rank's flags.  Peers then poll their own memory.
+__device__ __forceinline__ void publish(int64_t *ctl, int64_t *const *flags, int world,
+                                        int rank, int64_t R, uint64_t *stamps = nullptr) {
+    ctl[0] = R;
+    if (world > 1) {
+        __threadfence_system();
+        if (stamps) stamps[5] = gtimer();
+        for (int j = 0; j < world; ++j) st_relaxed_sys(flags[j] + rank, R);
+        if (stamps) stamps[6] = gtimer();
+    } else {
+        __threadfence();
+        atomicExch(reinterpret_cast<unsigned long long *>(flags[0]), (unsigned long long)R);
+    }
+}
+
+// Every local flag slot >= R (one thread).
+__device__ __forceinline__ void wait_flags(const int64_t *flags, int world, int64_t R) {
+    for (int j = 0; j < world; ++j)
+        while (ld_acquire_sys(flags + j) < R) __nanosleep(32);
+}
+
 // Finalize of a solve whose Delta v goes to the peer exchange: alpha += delta
 // (kept in the SVM box), dv_r[(R+1)&1] = (view - lin)/quad, the generator
 // jump, and — once every block is done — flag_r = R+1.
 __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     SolveState *st, const double *delta0, const double *delta1, const double *view0,
     const double *view1, const double *lin, double quad, int64_t m, int64_t d, double *alpha,
-    int box, double *dv, int64_t *ctl, int next_known, uint64_t next_state) {
+    int box, double *dv, int64_t *ctl, int64_t *const *flags, int world, int rank,
+    int next_known, uint64_t next_state) {
     __shared__ int s_last;
     const int dc = st->dc;
     const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
@@ -91,8 +132,7 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
         ctl[2] = 0;
-        __threadfence_system();
-        st_release_sys(ctl, R + 1);
+        publish(ctl, flags, world, rank, R + 1);
     }
 }
 
@@ -124,7 +164,7 @@ struct RoundStart {
     double K, L;
     int world;
     double *const *bufs;
-    int64_t *const *flags;
+    const int64_t *flags;      // local flag slots
     int64_t *ctl;
     SolveState *st;            // mode 2
     double *view0, *view1;
@@ -139,9 +179,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
         const int64_t R = p.ctl[0], C = p.ctl[1];
         s_R = R;
         s_apply = R > C;
-        if (R > C)
-            for (int j = 0; j < p.world; ++j)
-                while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(64);
+        if (R > C) wait_flags(p.flags, p.world, R);
     }
     __syncthreads();
     const int apply = s_apply;
@@ -231,9 +269,10 @@ struct TurnParams {
     double *alpha;
     int box, next_known;
     uint64_t next_state;
-    int world;
+    int world, rank;
     double *const *bufs;
-    int64_t *const *flags;
+    int64_t *const *flags;     // every rank's flag slots
+    const int64_t *flags_in;   // local flag slots
     int64_t *ctl;
     double *dv_own;
     int kind;
@@ -246,11 +285,6 @@ struct TurnParams {
     uint64_t *stamps;          // optional phase timestamps (globaltimer ns)
 };
 
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const int64_t *p) {
     uint64_t v;
@@ -295,13 +329,8 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
                 const double u = x - l;
                 acc[1] += l * u + 0.5 * u * u;
             }
-        if (p.stamps && blockIdx.x == 0) {
-            __syncthreads();
-            if (threadIdx.x == 0) p.stamps[5] = gtimer();
-        }
         block_sum<3>(acc, sm);
         if (threadIdx.x == 0) {
-            if (p.stamps && blockIdx.x == 0) p.stamps[6] = gtimer();
             p.partials[blockIdx.x * 3 + 1] = acc[1];
             p.partials[blockIdx.x * 3 + 2] = acc[2];
             __threadfence();
@@ -375,13 +404,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             if (s_last) {
                 p.ctl[2] = 0;
                 if (p.stamps) p.stamps[2] = gtimer();
-                if (p.world > 1) {          // peers read this flag over NVLink
-                    __threadfence_system();
-                    st_release_sys(p.ctl, s_R + 1);
-                } else {
-                    atomicExch(reinterpret_cast<unsigned long long *>(p.ctl),
-                               (unsigned long long)(s_R + 1));
-                }
+                publish(p.ctl, p.flags, p.world, p.rank, s_R + 1, p.stamps);
             }
         }
     }
@@ -389,16 +412,10 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     const int64_t R = s_R + 1;
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
-            // one poller per rank reads the peers' flags over NVLink, then
-            // releases a local "every rank published R" word (ctl[3]) that the
-            // other blocks poll in this GPU's L2
-            if (p.world > 1) {
-                for (int j = 0; j < p.world; ++j)
-                    while (ld_acquire_sys(p.flags[j]) < R) __nanosleep(32);
-            } else {
-                while ((int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl), 0ull) < R)
-                    __nanosleep(32);
-            }
+            // one poller per rank watches the local flag slots (the peers
+            // store into them over NVLink), then releases a local "every rank
+            // published R" word (ctl[3]) for the other blocks
+            wait_flags(p.flags_in, p.world, R);
             __threadfence();
             atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 3), (unsigned long long)R);
         } else {
@@ -467,7 +484,7 @@ int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, i
     blocks = blocks < 1 ? 1 : (blocks > 8 * NUM_SMS ? 8 * NUM_SMS : blocks);
     peer_finalize_kernel<<<(int)blocks, PEER_THREADS, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], lin, quad, m, d, alpha, box,
-        pr->dv, pr->ctl, next_known, next_state);
+        pr->dv, pr->ctl, pr->flags_dev, pr->world, pr->rank, next_known, next_state);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
@@ -496,6 +513,7 @@ int glm_peer_destroy(glm_peer *p) {
 int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) {
     if (!out || d < 0 || world < 1 || rank < 0 || rank >= world)
         return glm_set_error(GLM_USAGE, "bad peer arguments");
+    if (world > PEER_MAX_WORLD) return glm_set_error(GLM_USAGE, "peer exchange: world > 24");
     GLM_CUDA_TRY(cudaSetDevice(device));
     glm_peer *p = new (std::nothrow) glm_peer();
     if (!p) return glm_set_error(GLM_USAGE, "out of host memory");
@@ -516,9 +534,10 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
     }
     p->ctl = reinterpret_cast<int64_t *>(p->mem);
     p->dv = reinterpret_cast<double *>(p->mem + 256);
+    p->flags = p->ctl + 8;
     if (world == 1) {
         double *b = p->dv;
-        int64_t *f = p->ctl;
+        int64_t *f = p->flags;
         GLM_CUDA_TRY(cudaMemcpy(p->bufs_dev, &b, sizeof(b), cudaMemcpyHostToDevice));
         GLM_CUDA_TRY(cudaMemcpy(p->flags_dev, &f, sizeof(f), cudaMemcpyHostToDevice));
     }
@@ -553,7 +572,7 @@ int glm_peer_open(glm_peer *p, const void *handles) {
             p->opened.push_back(q);
             base = (char *)q;
         }
-        flags[j] = reinterpret_cast<int64_t *>(base);
+        flags[j] = reinterpret_cast<int64_t *>(base) + 8;
         bufs[j] = reinterpret_cast<double *>(base + 256);
     }
     GLM_CUDA_TRY(cudaMemcpy(p->bufs_dev, bufs.data(), sizeof(double *) * p->world,
@@ -603,7 +622,7 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
     a.L = n_devices;
     a.world = p->world;
     a.bufs = p->bufs_dev;
-    a.flags = p->flags_dev;
+    a.flags = p->flags;
     a.ctl = p->ctl;
     a.st = s ? s->st : nullptr;
     a.view0 = s ? s->view[0] : nullptr;
@@ -647,8 +666,10 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
     a.next_known = s->host_known ? 1 : 0;
     a.next_state = s->host_gen;
     a.world = p->world;
+    a.rank = p->rank;
     a.bufs = p->bufs_dev;
     a.flags = p->flags_dev;
+    a.flags_in = p->flags;
     a.ctl = p->ctl;
     a.dv_own = p->dv;
     a.kind = kind;

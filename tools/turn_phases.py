@@ -1,7 +1,8 @@
 """Phase timestamps of glm_round_turn on the C2 workload (debug); world >= 1
-under torchrun. Prints, per rank, the median µs of: P1 decide | P2 publish |
-wait for every rank | P3 round start | block-0 view loads | block-0 reduced |
-last block starts its fold."""
+under torchrun; 3-round CUDA graphs replayed like bench.py, stamps of the
+last round's turn. Prints, per rank, the median µs of: P1 decide | P2 publish |
+wait for every rank | P3 round start | publish: system fence done | flag
+stores issued | last block starts its P1 fold (all relative to the turn start)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -26,11 +27,17 @@ st = torch.zeros(8, dtype=torch.int64, device="cuda")
 L.check(L.lib().glm_peer_stamps(eng.exchange.handle, st.data_ptr()), "stamps")
 for _ in range(5):
     eng.outer_round()
+torch.cuda.synchronize()
+eng.reset()
+graph = eng.capture(3)           # graph replay like bench.py: no host pacing between rounds
 ph = []
+raw = []
 for _ in range(40):
-    eng.outer_round()
+    eng.reset()
+    graph.replay()
     torch.cuda.synchronize()
     s = st.cpu().numpy().astype(np.int64)
+    raw.append(s.copy())
     ph.append(np.concatenate([np.diff(s[:5]), [s[5] - s[0], s[6] - s[0], s[7] - s[0]]]) / 1e3)
 med = torch.tensor(np.median(ph, axis=0), device="cuda")
 out = [torch.zeros_like(med) for _ in range(world)]
@@ -41,5 +48,17 @@ else:
 if rank == 0:
     for r, o in enumerate(out):
         print(f"rank {r}:", np.round(o.cpu().numpy(), 2), flush=True)
+# %globaltimer is not synchronised across GPUs, so the skew is read from the
+# local waits (publish -> every flag seen): per replay the last rank to publish
+# waits only for the flag latency, the others also for that rank.
+if world > 1:
+    wt = torch.tensor([(x[3] - x[2]) / 1e3 for x in raw], dtype=torch.float64, device="cuda")
+    allw = [torch.zeros_like(wt) for _ in range(world)]
+    dist.all_gather(allw, wt)
+    if rank == 0:
+        W = np.stack([x.cpu().numpy() for x in allw])        # [rank, replay]
+        print("wait per replay (us): median of min over ranks (flag latency):",
+              round(float(np.median(W.min(0))), 2), "| median of max over ranks:",
+              round(float(np.median(W.max(0))), 2))
 sys.stdout.flush()
 os._exit(0)
