@@ -316,6 +316,8 @@ int or_step_from_ga(int kind, double lam, double rho, double y, double ga, doubl
         return OR_OK;
     }
     case 0: {
+        /* math.log(t / (1 - t)) raises outside (0, 1) (solver.py:181) */
+        if (!(t > 0.0 && t < 1.0)) return OR_SOLVER_ERROR;
         double grad = ga + log(t / (1.0 - t));
         double curv = c + 1.0 / (t * (1.0 - t));
         double tn = t - grad / curv;

@@ -451,6 +451,7 @@ struct glm_ctx {
     double *lin = nullptr, *base = nullptr, *y = nullptr, *cnst = nullptr;
     double *dalpha = nullptr, *dv = nullptr, *alpha = nullptr, *v = nullptr, *w = nullptr;
     double *tgt = nullptr, *out4 = nullptr, *scratch = nullptr;
+    double *pin_cnst = nullptr;   // pinned host staging for the scalar input
 };
 
 int glm_ctx_destroy(glm_ctx *c) {
@@ -463,6 +464,7 @@ int glm_ctx_destroy(glm_ctx *c) {
     void *ptrs[] = {c->indptr, c->rows, c->vals, c->sq, c->lin, c->base, c->y, c->cnst,
                     c->dalpha, c->dv, c->alpha, c->v, c->w, c->tgt, c->out4, c->scratch};
     for (void *p : ptrs) cudaFree(p);
+    if (c->pin_cnst) cudaFreeHost(c->pin_cnst);
     if (c->stream) cudaStreamDestroy(c->stream);
     cudaSetDevice(prev);
     delete c;
@@ -493,6 +495,7 @@ int glm_ctx_create(int device, int layout, int64_t n_rows, int64_t n_cols, const
     chk(cudaMalloc(&c->cnst, sizeof(double) * 8));
     chk(cudaMalloc(&c->out4, sizeof(double) * 8));
     chk(cudaMalloc(&c->scratch, REDUCE_SCRATCH_BYTES));
+    chk(cudaMallocHost(&c->pin_cnst, sizeof(double)));
     if (e == cudaSuccess) {
         chk(cudaMemsetAsync(c->scratch, 0, REDUCE_SCRATCH_BYTES, c->stream));
         if (layout == GLM_CSC) {
@@ -547,7 +550,8 @@ int glm_device_solve(glm_ctx *c, int kind, double lam, double l1_ratio,
     if (m > 0) GLM_CUDA_TRY(cudaMemcpyAsync(c->base, base, sizeof(double) * m, cudaMemcpyHostToDevice, s));
     if (coord_target && m > 0)
         GLM_CUDA_TRY(cudaMemcpyAsync(c->y, coord_target, sizeof(double) * m, cudaMemcpyHostToDevice, s));
-    GLM_CUDA_TRY(cudaMemcpyAsync(c->cnst, &cnst, sizeof(double), cudaMemcpyHostToDevice, s));
+    *c->pin_cnst = cnst;              // pinned: the copy never stages through pageable memory
+    GLM_CUDA_TRY(cudaMemcpyAsync(c->cnst, c->pin_cnst, sizeof(double), cudaMemcpyHostToDevice, s));
     int rc = set_state(c->solver, *gen_state_io, *damping_io, s);
     if (rc) return rc;
     glm_solve_args a{};
@@ -565,14 +569,14 @@ int glm_device_solve(glm_ctx *c, int kind, double lam, double l1_ratio,
     a.group_lanes = 0;
     a.reset_damping = 0;
     glm_solve_result r{};
-    rc = solve(c->solver, &c->A, &a, c->dalpha, c->dv, nullptr, s);
+    HostCopies hc;
+    hc.delta = dalpha_out;
+    hc.dv = dv_out;
+    // one host round trip when the batch is accepted: finalize and the copies
+    // are enqueued before the solve's synchronisation (solve's HostCopies)
+    rc = solve(c->solver, &c->A, &a, c->dalpha, c->dv, &r, s, &hc);
     if (rc) return rc;
-    if (dalpha_out && m > 0)
-        GLM_CUDA_TRY(cudaMemcpyAsync(dalpha_out, c->dalpha, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
-    if (dv_out && d > 0)
-        GLM_CUDA_TRY(cudaMemcpyAsync(dv_out, c->dv, sizeof(double) * d, cudaMemcpyDeviceToHost, s));
-    rc = read_result(c->solver, &r, values_out, epochs, s);
-    if (rc) return rc;
+    if (values_out) fill_result(c->solver, nullptr, values_out, epochs);
     *gen_state_io = r.gen_state;
     *damping_io = r.damping;
     if (info_out) {

@@ -216,6 +216,9 @@ __device__ __forceinline__ bool coord_step(int kind, double lam, double rho, dou
         step = -(ga + t - y) / (c + 1.0);
         return true;
     case GLM_DUAL_L2_LOGISTIC: {
+        // math.log / the division raise for t outside (0, 1) (solver.py:181);
+        // reachable only with a caller-held damping above 1
+        if (!(t > 0.0 && t < 1.0)) return false;
         double grad = ga + log(t / (1.0 - t));
         double curv = c + 1.0 / (t * (1.0 - t));
         double tn = t - grad / curv;

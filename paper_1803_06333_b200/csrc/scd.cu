@@ -1142,6 +1142,11 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
     GLM_CUDA_TRY(cudaMemcpyAsync(s->st_host, s->st, sizeof(SolveState), cudaMemcpyDeviceToHost,
                                  stream));
     GLM_CUDA_TRY(cudaStreamSynchronize(stream));
+    fill_result(s, res, epoch_values, cap);
+    return GLM_OK;
+}
+
+void fill_result(const glm_solver *s, glm_solve_result *res, double *epoch_values, int cap) {
     const SolveState &h = *s->st_host;
     if (res) {
         res->status = h.status;
@@ -1160,11 +1165,10 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
         n = n < MAX_EPOCH_VALUES ? n : MAX_EPOCH_VALUES;
         for (int i = 0; i < n; ++i) epoch_values[i] = h.epoch_values[i];
     }
-    return GLM_OK;
 }
 
 int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *delta_out,
-          double *dv_out, glm_solve_result *res, cudaStream_t stream) {
+          double *dv_out, glm_solve_result *res, cudaStream_t stream, const HostCopies *hc) {
     if (!A || !a) return glm_set_error(GLM_USAGE, "null matrix or args");
     if (a->epochs < 1) return glm_set_error(GLM_USAGE, "t_epochs must be >= 1");
     const int64_t m = A->n_cols, d = A->n_rows;
@@ -1360,6 +1364,29 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         return GLM_OK;
     };
 
+    const bool peer_fin = (a->flags & GLM_FLAG_PEER_FINALIZE) && a->peer && a->accumulate &&
+                          delta_out;
+    auto plain_finalize = [&]() -> int {
+        count_launch();
+        finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
+            s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
+            delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0, early ? 1 : 0,
+            next_state);
+        GLM_CUDA_TRY(cudaGetLastError());
+        return GLM_OK;
+    };
+    // outputs enqueued before the adaptive loop's synchronisation (see HostCopies)
+    const bool spec = hc && !turn && !peer_fin && !a->accumulate && !s->timing && m > 0;
+    auto copies = [&]() -> int {
+        if (hc->delta && delta_out)
+            GLM_CUDA_TRY(cudaMemcpyAsync(hc->delta, delta_out, sizeof(double) * m,
+                                         cudaMemcpyDeviceToHost, stream));
+        if (hc->dv && dv_out && d > 0)
+            GLM_CUDA_TRY(cudaMemcpyAsync(hc->dv, dv_out, sizeof(double) * d,
+                                         cudaMemcpyDeviceToHost, stream));
+        return GLM_OK;
+    };
+    bool finalized = false;
     if (m > 0) {
         if (a->max_attempts > 0) {
             for (int i = 0; i < a->max_attempts; ++i)
@@ -1369,9 +1396,13 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             for (;;) {
                 for (int i = 0; i < batch; ++i)
                     if ((rc = attempt())) return rc;
+                if (spec && ((rc = plain_finalize()) || (rc = copies()))) return rc;
                 glm_solve_result r;
                 if ((rc = read_result(s, &r, nullptr, 0, stream))) return rc;
-                if (r.done) break;
+                if (r.done) {
+                    finalized = spec;
+                    break;
+                }
                 batch = a->epochs - r.epochs_run;
                 if (batch < 1) batch = 1;
             }
@@ -1382,24 +1413,21 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         count_launch();
         empty_solve_kernel<<<1, 1, 0, stream>>>(s->st);
     }
-    if (turn) {
-        // value, finalize and the exchange run in glm_round_turn
+    if (turn || finalized) {
+        // turn: value, finalize and the exchange run in glm_round_turn;
+        // finalized: the speculative finalize + copies were the last ones
     } else if (s->timing && (rc = glue_begin(s, 0, stream))) {
         return rc;
-    } else if ((a->flags & GLM_FLAG_PEER_FINALIZE) && a->peer && a->accumulate && delta_out) {
+    } else if (peer_fin) {
         // Delta v goes to this rank's peer-exchange buffer (peer.cu)
         rc = peer_finalize(s, a->peer, a->lin, a->quad, m, d, delta_out,
                            a->kind == GLM_DUAL_L2_SVM ? 1 : 0, early ? 1 : 0, next_state, stream);
         if (rc) return rc;
     } else {
-        count_launch();
-        finalize_kernel<<<grid_stride_blocks(m > d ? m : d), 256, 0, stream>>>(
-            s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], a->lin, a->quad, m, d,
-            delta_out, dv_out, a->accumulate, a->kind == GLM_DUAL_L2_SVM ? 1 : 0, early ? 1 : 0,
-            next_state);
-        GLM_CUDA_TRY(cudaGetLastError());
+        if ((rc = plain_finalize())) return rc;
+        if (hc && (rc = copies())) return rc;
     }
-    if (!turn && s->timing && (rc = glue_end(s, stream))) return rc;
+    if (!turn && !finalized && s->timing && (rc = glue_end(s, stream))) return rc;
     s->last_epochs = a->epochs;
     s->last_m = m;
     if (early) {
@@ -1420,7 +1448,13 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             s->prefetch_alt = false;
         }
     }
-    if (res) return read_result(s, res, nullptr, 0, stream);
+    if (res) {
+        if (finalized) {                      // the loop's copy of the state is final
+            fill_result(s, res, nullptr, 0);
+            return GLM_OK;
+        }
+        return read_result(s, res, nullptr, 0, stream);
+    }
     return GLM_OK;
 }
 

@@ -46,10 +46,22 @@ namespace glm {
 constexpr int VALUE_THREADS = 256;
 constexpr size_t REDUCE_SCRATCH_BYTES = 64 * 1024;
 
+// Host destinations of the solve's outputs (glm_device_solve): with these the
+// adaptive solve enqueues finalize + the copies after each batch of attempts,
+// before its one synchronisation, so an accepted batch costs a single host
+// round trip (a rejected one re-runs the idempotent finalize and copies).
+struct HostCopies {
+    double *delta = nullptr;   // f64[m]
+    double *dv = nullptr;      // f64[d]
+};
+
 int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *delta_out,
-          double *dv_out, glm_solve_result *res, cudaStream_t stream);
+          double *dv_out, glm_solve_result *res, cudaStream_t stream,
+          const HostCopies *hc = nullptr);
 int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int cap,
                 cudaStream_t stream);
+// fill res / epoch_values from the state last copied to the host
+void fill_result(const glm_solver *s, glm_solve_result *res, double *epoch_values, int cap);
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
 int join_prefetch(glm_solver *s, cudaStream_t stream);
 // record the start of a timed glue kernel (returns the pair to close with glue_end)

@@ -225,6 +225,64 @@ def test_gpu_chunk_runner_drop_in(golden):
     runner.close()
 
 
+def test_gpu_chunk_runner_retries_vs_oracle(golden):
+    """Rejected attempts through glm_device_solve: a caller-held damping above 1
+    overshoots, the solve rolls back, halves and retries (solver.py:281-300);
+    the single-synchronisation path re-runs finalize and the copies after each
+    extra batch.  Sequential mode against the oracle's damped_solve.  The ridge
+    cases are left out: after the overshoot they sit at the optimum, where the
+    plateau test (G increase <= 1e-12 relative, solver.py:247) compares values
+    that differ only in summation order."""
+    z = golden("solve")
+    runner = g.gpu_chunk_runner()
+
+    class Dev:
+        pass
+
+    class Cfg:
+        threads_per_device = 1
+
+    seen_retries = 0
+    for c in range(int(z["n_cases"])):
+        p = f"c{c}_"
+        m = _mat(z, p)
+        tgt = z[p + "target"]
+        kind = KINDS[int(z[p + "kind"])]
+        if kind == "ridge_primal":
+            continue
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]), 1, 1,
+                               target=tgt if len(tgt) else None)
+        for damping in (4.0, 64.0):
+            sub = g.LocalSubproblem(spec=spec, lin=z[p + "lin"], quad=float(z[p + "quad"]),
+                                    const=float(z[p + "const"]), base=z[p + "base"], data=m,
+                                    col_ids=np.arange(m.n_cols))
+            dev = Dev()
+            dev.gen = g.PermutationGenerator(int(z[p + "gen_seed"]))
+            dev.damping = g.DampingState(delta=damping)
+            cfg = Cfg()
+            cfg.epochs = int(z[p + "epochs"])
+            om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+            y = getattr(spec, "coord_target", None)
+            want = oracle.damped_solve(kind, spec.lam, om, sub.lin, sub.quad, sub.const,
+                                       sub.base, int(z[p + "gen_seed"]) or 0, cfg.epochs,
+                                       damping=damping, y=None if y is None else np.asarray(y))
+            if want["status"] != 0:
+                with pytest.raises(Exception):
+                    runner(sub, dev, cfg)
+                continue
+            res = runner(sub, dev, cfg)
+            assert res.retries == want["retries"]
+            assert res.epochs_run == want["epochs_run"]
+            assert dev.damping.delta == want["damping"]
+            assert dev.gen.state == want["gen_state"]
+            np.testing.assert_allclose(res.epoch_values, want["values"], rtol=1e-11)
+            np.testing.assert_allclose(res.delta_alpha, want["delta"], atol=1e-9)
+            np.testing.assert_allclose(res.delta_v, want["dv"], atol=1e-9)
+            seen_retries += res.retries
+    assert seen_retries > 0
+    runner.close()
+
+
 def test_zero_column_and_empty_edge_cases():
     # lasso zero column: step -t (test_solver.py:83-87)
     spec = g.ObjectiveSpec("lasso_primal", 0.5, 3, 1, target=np.zeros(3))
