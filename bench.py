@@ -550,7 +550,7 @@ def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world
         _lib.check(int(out[7]), "glm_device_solve")
         tb = time.perf_counter()
         if reducer is not None:
-            reducer.allreduce_sum(dvb)
+            reducer.allreduce_sum(dvb, out=dvb)
         t_solve.append(tb - ta)
         t_red.append(time.perf_counter() - tb)
     el = time.perf_counter() - t0

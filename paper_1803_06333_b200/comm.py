@@ -140,22 +140,24 @@ class NcclReducer:
         if self._aborted:
             raise ReduceError("collective aborted")
         t, was_tensor = self._tensor(vec)
-        n = torch.tensor([t.numel()], dtype=torch.int64, device=self.device)
-        nmax, nmin = n.clone(), n.clone()
-        if self.world > 1:
-            dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=self.group)
-            dist.all_reduce(nmin, op=dist.ReduceOp.MIN, group=self.group)
-        if int(nmax.item()) != int(nmin.item()):
-            raise ProtocolError("vector length mismatch")
+        if self.world > 1:     # one collective checks the lengths: max(n) == -max(-n)
+            n = torch.tensor([t.numel(), -t.numel()], dtype=torch.int64, device=self.device)
+            dist.all_reduce(n, op=dist.ReduceOp.MAX, group=self.group)
+            hi, neg_lo = n.tolist()
+            if hi != -neg_lo:
+                raise ProtocolError("vector length mismatch")
         if self.deterministic:
-            parts = [torch.empty_like(t) for _ in range(self.world)]
-            dist.all_gather(parts, t, group=self.group)
-            res = canonical_sum(parts)      # ascending rank order
+            flat = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(flat, t, group=self.group)
+            res = canonical_sum(list(flat.view(self.world, -1)))   # ascending rank order
         else:
             res = t.clone()
             dist.all_reduce(res, op=dist.ReduceOp.SUM, group=self.group)
         if out is not None:
-            out.copy_(res)
+            if isinstance(out, np.ndarray):
+                torch.from_numpy(out).copy_(res)
+            else:
+                out.copy_(res)
             return out
         return res if was_tensor else res.cpu().numpy()
 

@@ -546,14 +546,17 @@ int glm_device_solve(glm_ctx *c, int kind, double lam, double l1_ratio,
     GLM_CUDA_TRY(cudaSetDevice(c->device));
     const int64_t m = c->A.n_cols, d = c->A.n_rows;
     cudaStream_t s = c->stream;
+    int rc = set_state(c->solver, *gen_state_io, *damping_io, s);
+    // attempt 0's permutation depends only on the generator state: build it
+    // on the side stream while the inputs cross PCIe
+    if (!rc) rc = prefetch_first_perm(c->solver, m, s);
+    if (rc) return rc;
     if (d > 0) GLM_CUDA_TRY(cudaMemcpyAsync(c->lin, lin, sizeof(double) * d, cudaMemcpyHostToDevice, s));
     if (m > 0) GLM_CUDA_TRY(cudaMemcpyAsync(c->base, base, sizeof(double) * m, cudaMemcpyHostToDevice, s));
     if (coord_target && m > 0)
         GLM_CUDA_TRY(cudaMemcpyAsync(c->y, coord_target, sizeof(double) * m, cudaMemcpyHostToDevice, s));
     *c->pin_cnst = cnst;              // pinned: the copy never stages through pageable memory
     GLM_CUDA_TRY(cudaMemcpyAsync(c->cnst, c->pin_cnst, sizeof(double), cudaMemcpyHostToDevice, s));
-    int rc = set_state(c->solver, *gen_state_io, *damping_io, s);
-    if (rc) return rc;
     glm_solve_args a{};
     a.kind = kind;
     a.mode = mode;

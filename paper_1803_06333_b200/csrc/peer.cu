@@ -15,6 +15,9 @@
 //                       canonical_sum on every rank); grad = f'(v); lin = grad;
 //                       view = lin; f(v); solver state reset (begin)
 //
+// The turn kernel writes Delta v speculatively while it evaluates the attempt
+// and publishes right at the damping decision; the flag word carries whether
+// the attempt was accepted (else the true Delta v is exactly zero).
 // dv_r lives in rank r's HBM, double-buffered by round parity; every rank
 // reads every peer's buffer through cudaIpc-mapped pointers (NVLink/NVSwitch).
 // A rank cannot overwrite dv_r[b] (round R+2) before every rank has consumed
@@ -31,9 +34,11 @@ struct glm_peer {
     // [ctl: 8 x i64 | flag slots: world x i64 | pad to 256 B | dv: 2 x d doubles]
     char *mem = nullptr;
     int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter,
-                                  // [3] "every rank published" (turn)
+                                  // [3] "every rank published" (turn), [4] their accept
+                                  // bits, [5] our last flag word
     int64_t *flags = nullptr;     // local slots: flags[j] = last round rank j published
-    double *dv = nullptr;
+    double *dv = nullptr;         // 2 halves of pstride doubles (Delta v[d], padded)
+    int64_t pstride = 0;
     double **bufs_dev = nullptr;  // world pointers to each rank's dv (device array)
     int64_t **flags_dev = nullptr;  // world pointers to each rank's flag slots
     std::vector<void *> opened;   // cudaIpc-opened peer allocations
@@ -46,6 +51,9 @@ namespace glm {
 constexpr int PEER_BLOCKS = 2 * NUM_SMS;
 constexpr int PEER_THREADS = 256;
 constexpr int PEER_MAX_WORLD = 24;      // flag slots that fit the 256-byte header
+
+// doubles per parity half: Delta v[d] padded to 256 B
+inline int64_t peer_pstride(int64_t d) { return ((d > 0 ? d : 1) + 1 + 31) / 32 * 32; }
 
 __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
     int64_t v;
@@ -69,26 +77,41 @@ __device__ __forceinline__ uint64_t gtimer() {
     return t;
 }
 
-// Publish round R (one thread, after every block's writes were fenced): our
-// slot in every rank's flags.  Peers then poll their own memory.
+// Flag word: R << 2 | accept bits; bit (R & 1) says whether round R's Delta v
+// is the attempt's (1) or exactly zero (0, a rejected attempt: the view went
+// back to the snapshot, which is lin).  Publishing R+1 keeps the bit of R, so
+// a peer still reading round R after we moved on sees the right one (we
+// cannot reach R+2 before that peer publishes R+1).  ctl[5] keeps our word.
+// One thread, after every block's writes were fenced: our slot in every
+// rank's flags; the peers then poll their own memory.
 __device__ __forceinline__ void publish(int64_t *ctl, int64_t *const *flags, int world,
-                                        int rank, int64_t R, uint64_t *stamps = nullptr) {
+                                        int rank, int64_t R, int accept,
+                                        uint64_t *stamps = nullptr) {
+    const int64_t keep = ctl[5] & (int64_t)(1 << ((R & 1) ^ 1));
+    const int64_t word = (R << 2) | keep | (int64_t)((accept ? 1 : 0) << (R & 1));
     ctl[0] = R;
+    ctl[5] = word;
     if (world > 1) {
         __threadfence_system();
         if (stamps) stamps[5] = gtimer();
-        for (int j = 0; j < world; ++j) st_relaxed_sys(flags[j] + rank, R);
+        for (int j = 0; j < world; ++j) st_relaxed_sys(flags[j] + rank, word);
         if (stamps) stamps[6] = gtimer();
     } else {
         __threadfence();
-        atomicExch(reinterpret_cast<unsigned long long *>(flags[0]), (unsigned long long)R);
+        atomicExch(reinterpret_cast<unsigned long long *>(flags[0]), (unsigned long long)word);
     }
 }
 
-// Every local flag slot >= R (one thread).
-__device__ __forceinline__ void wait_flags(const int64_t *flags, int world, int64_t R) {
-    for (int j = 0; j < world; ++j)
-        while (ld_acquire_sys(flags + j) < R) __nanosleep(32);
+// Every local flag slot at round >= R (one thread); returns the ranks'
+// accept bits of round R.
+__device__ __forceinline__ uint32_t wait_flags(const int64_t *flags, int world, int64_t R) {
+    uint32_t mask = 0;
+    for (int j = 0; j < world; ++j) {
+        int64_t f;
+        while (((f = ld_acquire_sys(flags + j)) >> 2) < R) __nanosleep(32);
+        mask |= (uint32_t)((f >> (R & 1)) & 1) << j;
+    }
+    return mask;
 }
 
 // Finalize of a solve whose Delta v goes to the peer exchange: alpha += delta
@@ -97,14 +120,14 @@ __device__ __forceinline__ void wait_flags(const int64_t *flags, int world, int6
 __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     SolveState *st, const double *delta0, const double *delta1, const double *view0,
     const double *view1, const double *lin, double quad, int64_t m, int64_t d, double *alpha,
-    int box, double *dv, int64_t *ctl, int64_t *const *flags, int world, int rank,
-    int next_known, uint64_t next_state) {
+    int box, double *dv, int64_t pstride, int64_t *ctl, int64_t *const *flags, int world,
+    int rank, int next_known, uint64_t next_state) {
     __shared__ int s_last;
     const int dc = st->dc;
     const double *dl = dc < 0 ? nullptr : (dc ? delta1 : delta0);
     const double *V = st->vw ? view1 : view0;
     const int64_t R = ctl[0];
-    double *out = dv + ((R + 1) & 1) * d;
+    double *out = dv + ((R + 1) & 1) * pstride;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if (dl) {
@@ -132,24 +155,26 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_finalize_kernel(
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
         ctl[2] = 0;
-        publish(ctl, flags, world, rank, R + 1);
+        publish(ctl, flags, world, rank, R + 1, 1);   // the solve's final Delta v
     }
 }
 
 // sum_j bufs[j][i] in ascending rank order (canonical_sum's bits): the (remote,
-// NVLink) loads of up to 8 ranks are issued together, then added in order.
-__device__ __forceinline__ double rank_sum(double *const *bufs, int world, int64_t i) {
+// NVLink) loads of up to 8 ranks are issued together, then added in order.  A
+// rank whose accept bit is 0 contributes +0.0 (its Delta v is exactly zero).
+__device__ __forceinline__ double rank_sum(double *const *bufs, int world, int64_t i,
+                                          uint32_t acc) {
     double s = 0.0;
     if (world <= 8) {
         double x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = j < world ? __ldcg(bufs[j] + i) : 0.0;
+        for (int j = 0; j < 8; ++j) x[j] = j < world && ((acc >> j) & 1) ? __ldcg(bufs[j] + i) : 0.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (j < world) s += x[j];
         return s;
     }
-    for (int j = 0; j < world; ++j) s += __ldcg(bufs[j] + i);
+    for (int j = 0; j < world; ++j) s += ((acc >> j) & 1) ? __ldcg(bufs[j] + i) : 0.0;
     return s;
 }
 
@@ -164,6 +189,7 @@ struct RoundStart {
     double K, L;
     int world;
     double *const *bufs;
+    int64_t pstride;
     const int64_t *flags;      // local flag slots
     int64_t *ctl;
     SolveState *st;            // mode 2
@@ -175,15 +201,17 @@ struct RoundStart {
 __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p) {
     __shared__ int s_apply;
     __shared__ int64_t s_R;
+    __shared__ uint32_t s_acc;
     if (threadIdx.x == 0) {
         const int64_t R = p.ctl[0], C = p.ctl[1];
         s_R = R;
         s_apply = R > C;
-        if (R > C) wait_flags(p.flags, p.world, R);
+        s_acc = R > C ? wait_flags(p.flags, p.world, R) : 0u;
     }
     __syncthreads();
     const int apply = s_apply;
-    const int64_t off = (s_R & 1) * p.d;
+    const int64_t off = (s_R & 1) * p.pstride;
+    const uint32_t accm = s_acc;
     double acc[1] = {0.0};
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -191,7 +219,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
     for (int64_t r = tid; r < p.d; r += nth) {
         double x = p.v[r];
         if (apply) {
-            x += rank_sum(p.bufs, p.world, off + r);
+            x += rank_sum(p.bufs, p.world, off + r, accm);
             p.v[r] = x;
         }
         if (p.mode == 0) continue;
@@ -247,16 +275,18 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
 
 // ---------------------------------------------------------------- turn
 // One kernel between two epochs (GLM_FLAG_TURN solves: one attempt each):
-//   P1  the attempt's value G and the damping decision (value_kernel mode 1)
-//   P2  finalize: alpha += delta, Delta v -> own exchange buffer, publish
+//   P1  the attempt's value G and the damping decision (value_kernel mode 1);
+//       the same pass writes Delta v to this rank's exchange buffer, and the
+//       deciding block sets the accept word and publishes
+//   P2  alpha += delta of the accepted attempt (while the peers finish)
 //   P3  wait for every rank's Delta v, then the next round's start
 //       (round_start_kernel mode 2)
-// P1 -> P2 is a grid barrier on st->turn (the deciding block bumps it), P2 ->
+// P1 -> P2 is a grid barrier on st->turn (the deciding block bumps it), P1 ->
 // P3 is the ranks' publication flags (ours is released only after all our
-// blocks finished P2).  Blocks spin only on work that finishes independently
-// of them and the grid is small (2 blocks per SM), so every block becomes
-// resident.  Replaces value + finalize + round start: three kernel launches,
-// ramps and tails per round become one.
+// blocks arrived in P1).  Blocks spin only on work that finishes
+// independently of them and the grid is small (2 blocks per SM), so every
+// block becomes resident.  Replaces value + finalize + round start: three
+// kernel launches, ramps and tails per round become one.
 struct TurnParams {
     SolveState *st;
     double *view0, *view1;
@@ -275,6 +305,7 @@ struct TurnParams {
     const int64_t *flags_in;   // local flag slots
     int64_t *ctl;
     double *dv_own;
+    int64_t pstride;
     int kind;
     double lam;
     const double *tgt;
@@ -305,7 +336,8 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     __shared__ int s_last;
     __shared__ uint32_t s_turn0;
     __shared__ int64_t s_R;
-    __shared__ int s_dc, s_vw;
+    __shared__ int s_dc;
+    __shared__ uint32_t s_acc;
     SolveState *st = p.st;
     volatile SolveState *vst = st;
     tl_start(TL_TURN);
@@ -318,22 +350,29 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     const bool active = !vst->done;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    // ---- P1: value of the attempt
+    double *out = p.dv_own + ((s_R + 1) & 1) * p.pstride;
+    // ---- P1: value of the attempt; Delta v = (view - lin)/quad goes to the
+    // exchange buffer on the same pass (the loads are shared).  If the attempt
+    // is rejected the view reverts to the snapshot, which is lin, so the true
+    // Delta v is exactly zero: the accept word tells the peers to add +0.0.
     {
-        const double *V = vst->vw ? p.view1 : p.view0;
+        const int vw0 = vst->vw;
+        const double *V = vw0 ? p.view1 : p.view0;
         double acc[3] = {0.0, 0.0, 0.0};
-        if (active)
-            for (int64_t r = tid; r < p.d; r += nth) {
-                const double x = V[r], l = p.lin[r];
+        for (int64_t r = tid; r < p.d; r += nth) {
+            const double x = __ldcg(V + r), l = p.lin[r];
+            const double u = x - l;
+            out[r] = u / p.quad;
+            if (active) {
                 if (!isfinite(x)) acc[2] += 1.0;
-                const double u = x - l;
                 acc[1] += l * u + 0.5 * u * u;
             }
+        }
         block_sum<3>(acc, sm);
         if (threadIdx.x == 0) {
             p.partials[blockIdx.x * 3 + 1] = acc[1];
             p.partials[blockIdx.x * 3 + 2] = acc[2];
-            __threadfence();
+            __threadfence();        // partials and Delta v before the arrival
             s_last = atomicAdd(&st->block_counter, 1u) == gridDim.x - 1;
         }
         __syncthreads();
@@ -355,24 +394,24 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             if (threadIdx.x == 0) {
                 st->block_counter = 0;
                 if (active) decide_attempt(st, *p.cnst + tot[1] / p.quad + gs[0], gs[0], tot[2], 0);
+                const int accept = st->vw == vw0;
                 __threadfence();
                 if (p.stamps) p.stamps[1] = gtimer();
-                atomicAdd(&st->turn, 1u);
+                atomicAdd(&st->turn, 1u);          // the other blocks go on to alpha
+                if (p.stamps) p.stamps[2] = gtimer();
+                publish(p.ctl, p.flags, p.world, p.rank, s_R + 1, accept, p.stamps);
             }
         }
         if (threadIdx.x == 0) {
             while (ld_acquire_gpu_u32(&st->turn) == s_turn0) __nanosleep(32);
             s_dc = vst->dc;
-            s_vw = vst->vw;
         }
         __syncthreads();
     }
-    // ---- P2: finalize + publish
+    // ---- P2: alpha += delta of the accepted attempt (overlaps the peers)
     {
         const int dc = s_dc;
         const double *dl = dc < 0 ? nullptr : (dc ? p.delta1 : p.delta0);
-        const double *V = s_vw ? p.view1 : p.view0;
-        double *out = p.dv_own + ((s_R + 1) & 1) * p.d;
         if (dl) {   // 4 independent rows per thread and pass: keep loads in flight
             for (int64_t j0 = tid; j0 < p.m; j0 += 4 * nth) {
                 double a[4], x[4];
@@ -389,23 +428,11 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
                 }
             }
         }
-        for (int64_t r = tid; r < p.d; r += nth) out[r] = (__ldcg(V + r) - p.lin[r]) / p.quad;
         if (blockIdx.x == 0 && threadIdx.x < 32) {
             const uint64_t g = p.next_known
                                    ? p.next_state
                                    : warp_jump(vst->gen_state, (uint64_t)vst->attempts * (uint64_t)p.m);
             if (threadIdx.x == 0) st->gen_next = g;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            s_last = atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl + 2), 1ull) ==
-                     (unsigned long long)(gridDim.x - 1);
-            if (s_last) {
-                p.ctl[2] = 0;
-                if (p.stamps) p.stamps[2] = gtimer();
-                publish(p.ctl, p.flags, p.world, p.rank, s_R + 1, p.stamps);
-            }
         }
     }
     // ---- P3: every rank's Delta v, then the next round's start
@@ -414,21 +441,26 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         if (blockIdx.x == 0) {
             // one poller per rank watches the local flag slots (the peers
             // store into them over NVLink), then releases a local "every rank
-            // published R" word (ctl[3]) for the other blocks
-            wait_flags(p.flags_in, p.world, R);
+            // published R" word (ctl[3]) and their accept bits (ctl[4]) for the
+            // other blocks
+            const uint32_t mask = wait_flags(p.flags_in, p.world, R);
+            s_acc = mask;
+            p.ctl[4] = (int64_t)mask;
             __threadfence();
             atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 3), (unsigned long long)R);
         } else {
             while ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) < R) __nanosleep(32);
+            s_acc = (uint32_t)*(volatile int64_t *)(p.ctl + 4);
         }
     }
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[3] = gtimer();
     __syncthreads();
-    const int64_t off = (R & 1) * p.d;
+    const int64_t off = (R & 1) * p.pstride;
+    const uint32_t accm = s_acc;
     double acc[1] = {0.0};
     const bool dual = kind_is_dual(p.kind);
     for (int64_t r = tid; r < p.d; r += nth) {
-        const double s = rank_sum(p.bufs, p.world, off + r);
+        const double s = rank_sum(p.bufs, p.world, off + r, accm);
         const double x = p.v[r] + s;
         p.v[r] = x;
         double f, g;
@@ -484,7 +516,7 @@ int peer_finalize(glm_solver *s, glm_peer *pr, const double *lin, double quad, i
     blocks = blocks < 1 ? 1 : (blocks > 8 * NUM_SMS ? 8 * NUM_SMS : blocks);
     peer_finalize_kernel<<<(int)blocks, PEER_THREADS, 0, stream>>>(
         s->st, s->delta[0], s->delta[1], s->view[0], s->view[1], lin, quad, m, d, alpha, box,
-        pr->dv, pr->ctl, pr->flags_dev, pr->world, pr->rank, next_known, next_state);
+        pr->dv, pr->pstride, pr->ctl, pr->flags_dev, pr->world, pr->rank, next_known, next_state);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
@@ -521,7 +553,8 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
     p->rank = rank;
     p->world = world;
     p->d = d;
-    const size_t bytes = 256 + sizeof(double) * 2 * (size_t)(d > 0 ? d : 1);
+    p->pstride = peer_pstride(d);
+    const size_t bytes = 256 + sizeof(double) * 2 * (size_t)p->pstride;
     cudaError_t e = cudaMalloc(&p->mem, bytes);
     if (e == cudaSuccess) e = cudaMemset(p->mem, 0, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->bufs_dev, sizeof(double *) * world);
@@ -622,6 +655,7 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
     a.L = n_devices;
     a.world = p->world;
     a.bufs = p->bufs_dev;
+    a.pstride = p->pstride;
     a.flags = p->flags;
     a.ctl = p->ctl;
     a.st = s ? s->st : nullptr;
@@ -672,6 +706,7 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
     a.flags_in = p->flags;
     a.ctl = p->ctl;
     a.dv_own = p->dv;
+    a.pstride = p->pstride;
     a.kind = kind;
     a.lam = lam;
     a.tgt = target;

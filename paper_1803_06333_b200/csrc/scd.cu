@@ -1124,6 +1124,35 @@ int join_prefetch(glm_solver *s, cudaStream_t stream) {
     return GLM_OK;
 }
 
+static int ensure_side_stream(glm_solver *s) {
+    if (!s->side) {
+        // the permutation prefetch runs at the lowest priority so the
+        // caller's round kernels (epoch, turn) get free SMs first
+        int lo = 0, hi = 0;
+        GLM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        GLM_CUDA_TRY(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, lo));
+        GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+        GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+    return GLM_OK;
+}
+
+int prefetch_first_perm(glm_solver *s, int64_t m, cudaStream_t stream) {
+    if (!s->host_known || m <= 0 || m > s->max_coords || s->prefetched) return GLM_OK;
+    int rc = ensure_device_tables();
+    if (rc || (rc = ensure_side_stream(s))) return rc;
+    GLM_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+    GLM_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    const PermScratch ps = carve_perm_scratch(s->perm_mem, s->max_coords, m);
+    int32_t *P = s->perm_cur ? s->perm_b : s->perm;
+    if ((rc = stream_perm(nullptr, s->host_gen, 0, m, P, ps, s->side))) return rc;
+    GLM_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
+    s->prefetched = true;
+    s->prefetch_m = m;
+    s->prefetch_alt = false;
+    return GLM_OK;
+}
+
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream) {
     int rc = join_prefetch(s, stream);
     if (rc) return rc;
@@ -1293,18 +1322,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     const bool turn = (a->flags & GLM_FLAG_TURN) && a->max_attempts == 1 && a->epochs == 1 &&
                       m > 0;
     const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
-    auto ensure_side = [&]() -> int {
-        if (!s->side) {
-            // the permutation prefetch runs at the lowest priority so the
-            // caller's round kernels (epoch, turn) get free SMs first
-            int lo = 0, hi = 0;
-            GLM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            GLM_CUDA_TRY(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, lo));
-            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
-            GLM_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
-        }
-        return GLM_OK;
-    };
+    auto ensure_side = [&]() -> int { return ensure_side_stream(s); };
     int launched = 0;
     auto attempt = [&]() -> int {
         // optional CUDA-event bracket: [perm | snapshot+epoch | value]

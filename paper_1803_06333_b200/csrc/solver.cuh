@@ -63,6 +63,9 @@ int read_result(glm_solver *s, glm_solve_result *res, double *epoch_values, int 
 // fill res / epoch_values from the state last copied to the host
 void fill_result(const glm_solver *s, glm_solve_result *res, double *epoch_values, int cap);
 int set_state(glm_solver *s, uint64_t gen_state, double damping, cudaStream_t stream);
+// After set_state: generate the solve's attempt-0 permutation on the side
+// stream now (e.g. under the caller's host->device input copies).
+int prefetch_first_perm(glm_solver *s, int64_t m, cudaStream_t stream);
 int join_prefetch(glm_solver *s, cudaStream_t stream);
 // record the start of a timed glue kernel (returns the pair to close with glue_end)
 int glue_begin(glm_solver *s, int kind, cudaStream_t stream);

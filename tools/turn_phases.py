@@ -1,8 +1,9 @@
 """Phase timestamps of glm_round_turn on the C2 workload (debug); world >= 1
 under torchrun; 3-round CUDA graphs replayed like bench.py, stamps of the
-last round's turn. Prints, per rank, the median µs of: P1 decide | P2 publish |
-wait for every rank | P3 round start | publish: system fence done | flag
-stores issued | last block starts its P1 fold (all relative to the turn start)."""
+last round's turn. Prints, per rank, the median µs of: P1 decide | turn
+counter bumped | publish -> every flag seen | P3 round start | publish: system
+fence done | flag stores issued | last block starts its P1 fold (the last
+three relative to the turn start)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
