@@ -461,9 +461,11 @@ def ours_main(args):
             rounds += 1
             obj, gap = eng2.objective_and_gap()
         torch.cuda.synchronize()
-        ttt = {"seconds": time.perf_counter() - t0, "epochs": rounds,
+        host_s = time.perf_counter() - t0
+        ttt = {"seconds": host_s, "epochs": rounds,
                "target": "duality gap <= 1e-3 * |F| (certifies relative suboptimality)",
-               "final_gap": gap, "final_objective": obj, "includes_gap_checks": True}
+               "final_gap": gap, "final_objective": obj, "includes_gap_checks": True,
+               "timer": "host loop: eager rounds, gap read back to the host every round"}
         # held-out test loss (PAPER.md:178 75/25 split: 250k more examples of the
         # same distribution), scored like cmd_predict --eval (w = v / lambda,
         # modelio.py:57-95): at the 1e-3 target and after converging further
@@ -480,6 +482,10 @@ def ours_main(args):
                             "accuracy_at_target": ev_t["accuracy"],
                             "logloss_converged": ev_c["logloss"],
                             "converged_epochs": rounds + more, "converged_rel_gap": gap / abs(obj)}
+        graph_ttt = ttt_graph(eng2, rounds, world) if args.graph else None
+        if graph_ttt is not None:
+            ttt["host_loop"] = {"seconds": host_s, "epochs": rounds}
+            ttt.update(graph_ttt)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -506,6 +512,57 @@ def ours_main(args):
     sys.stdout.flush()
     sys.stderr.flush()
     os._exit(0)
+
+
+def ttt_graph(eng, rounds, world):
+    """Time to the 1e-3 target on the device: a trajectory of rounds + 4
+    rounds from alpha0 captured as one CUDA graph with the fused gap kernels
+    after every round (into per-round device slots) and a timing event after
+    each gap; the time is start -> the event after the first round whose
+    certified gap meets the target (gap checks included, no host round trips;
+    the rounds after it are not counted).  Max over ranks."""
+    import torch
+    K = rounds + 4
+    slots = torch.zeros((K + 1, 4), dtype=torch.float64, device="cuda")
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(K + 1)]
+
+    def on_round(r):
+        eng.gap_terms_async(slots[r])
+        evs[r].record()
+
+    try:
+        eng.reset()
+        graph = eng.capture(K, on_round=on_round)
+    except Exception as exc:   # pragma: no cover - capture unsupported
+        return {"graph_error": repr(exc)}
+    best = None
+    for _ in range(3):                           # warm replay, then timed ones
+        eng.reset()
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        graph.replay()
+        torch.cuda.synchronize()
+        h = slots.cpu().numpy()
+        obj = h[:, 3] + h[:, 1]
+        gap = h[:, 0] + h[:, 1] + h[:, 2]
+        hit = [r for r in range(K + 1) if gap[r] <= 1e-3 * abs(obj[r])]
+        if not hit:
+            continue
+        r = hit[0]
+        ms = max_over_ranks(t0.elapsed_time(evs[r]), world)
+        if best is None or ms < best[0]:
+            best = (ms, r, gap[r], obj[r])
+    if best is None:
+        return {"graph_error": f"target not reached within {K} graph rounds"}
+    return {"seconds": best[0] / 1e3, "epochs": int(best[1]), "final_gap": float(best[2]),
+            "final_objective": float(best[3]),
+            "timer": "device: CUDA events inside one graph replay (rounds + fused gap kernels "
+                     "after every round), best of 2 replays after a warm one, max over ranks"}
 
 
 def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world):

@@ -11,6 +11,21 @@ namespace glm {
 
 constexpr int RED_BLOCKS = 2 * NUM_SMS;
 constexpr int RED_THREADS = 256;
+// column passes (gap part B, predict) are gather-latency bound: one wave of
+// as many resident CTAs as the kernel's registers allow keeps the most
+// columns in flight (the reduction scratch holds up to 4096 CTA partials)
+template <class K>
+static int full_grid(K kernel) {
+    static int grid = 0;
+    if (!grid) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, RED_THREADS, 0) !=
+                cudaSuccess || per_sm < 1)
+            per_sm = 2;
+        grid = (per_sm > 8 ? 8 : per_sm) * NUM_SMS;
+    }
+    return grid;
+}
 
 // scratch layout: [u32 counter | pad 16B][partials RED_BLOCKS x NV]
 template <int NV>
@@ -165,6 +180,61 @@ __global__ void __launch_bounds__(RED_THREADS) gap_rows_kernel(int kind, double 
     }
 }
 
+// a_j.w by the G lanes of a column group: each lane takes every G-th entry;
+// four entries per lane are loaded (indices, values, then the gathers) before
+// any is added, in the same order as a plain strided loop.
+template <int G, bool DENSE>
+__device__ __forceinline__ double column_dot(int64_t lo, int64_t hi, int gl, const int32_t *rows,
+                                             const double *vals, const double *w) {
+    double dot = 0.0;
+    for (int64_t q0 = lo + gl; q0 < hi; q0 += 4 * G) {
+        int r[4];
+        double a[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = q0 + (int64_t)u * G;
+            r[u] = q < hi ? (DENSE ? (int)(q - lo) : __ldg(rows + q)) : -1;
+            a[u] = q < hi ? __ldg(vals + q) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = r[u] >= 0 ? w[r[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (r[u] >= 0) dot += a[u] * x[u];
+    }
+    return group_sum<G>(dot);
+}
+
+// One warp, 32 consecutive columns cb..cb+31: lane L loads the bounds of
+// column cb+L (coalesced), the G-lane groups take the columns GPW at a time
+// (bounds handed over by shuffles, no dependent indptr load per column), and
+// every dot lands in the lane of its column, so the per-column epilogue
+// (transcendentals, loads of alpha / labels) runs on all 32 lanes.
+template <int G, bool DENSE>
+__device__ __forceinline__ double warp_column_dots(int64_t cb, int64_t n, int64_t d,
+                                                   const int64_t *indptr, const int32_t *rows,
+                                                   const double *vals, const double *w) {
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    int64_t mlo = 0, mhi = 0;
+    const int64_t jm = cb + lane;
+    if (jm < n) {
+        if (DENSE) { mlo = jm * d; mhi = mlo + d; }
+        else { mlo = __ldg(indptr + jm); mhi = __ldg(indptr + jm + 1); }
+    }
+    double mine = 0.0;
+#pragma unroll 4
+    for (int it = 0; it < G; ++it) {
+        const int src = it * GPW + sub;
+        const int64_t lo = __shfl_sync(0xffffffffu, mlo, src);
+        const int64_t hi = __shfl_sync(0xffffffffu, mhi, src);
+        const double dot = column_dot<G, DENSE>(lo, hi, gl, rows, vals, w);
+        const double v = __shfl_sync(0xffffffffu, dot, (lane % GPW) * G);
+        if (lane / GPW == it) mine = v;
+    }
+    return mine;
+}
+
 // gap part B over the columns: s_j = -a_j.w; g(alpha_j) + g*(s_j)
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(RED_THREADS) gap_cols_kernel(
@@ -172,25 +242,13 @@ __global__ void __launch_bounds__(RED_THREADS) gap_cols_kernel(
     const int64_t *indptr, const int32_t *rows, const double *vals, const double *alpha,
     const double *w, double *out, double *scratch) {
     double acc[2] = {0.0, 0.0};
-    constexpr int GPW = 32 / G;
-    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t jb = warp * GPW; jb < n; jb += nwarps * GPW) {
-        const int64_t j = jb + sub;
-        const bool valid = j < n;
-        int64_t lo = 0, hi = 0;
-        if (valid) {
-            if (DENSE) { lo = j * d; hi = lo + d; }
-            else { lo = indptr[j]; hi = indptr[j + 1]; }
-        }
-        double dot = 0.0;
-        for (int64_t q = lo + gl; q < hi; q += G) {
-            const int r = DENSE ? (int)(q - lo) : rows[q];
-            dot += vals[q] * w[r];
-        }
-        dot = group_sum<G>(dot);
-        if (valid && gl == 0) {
+    for (int64_t cb = warp * 32; cb < n; cb += nwarps * 32) {
+        const double dot = warp_column_dots<G, DENSE>(cb, n, d, indptr, rows, vals, w);
+        const int64_t j = cb + lane;
+        if (j < n) {
             const double yj = y ? y[j] : 0.0;
             acc[0] += g_one(kind, lam, rho, yj, alpha[j]);
             acc[1] += g_conj_one(kind, lam, rho, yj, -dot);
@@ -220,25 +278,13 @@ __global__ void __launch_bounds__(RED_THREADS) predict_kernel(
     const double *w, const double *y, int classify, double *scores, double *prob, double *out,
     double *scratch) {
     double acc[3] = {0.0, 0.0, 0.0};
-    constexpr int GPW = 32 / G;
-    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t jb = warp * GPW; jb < n; jb += nwarps * GPW) {
-        const int64_t j = jb + sub;
-        const bool valid = j < n;
-        int64_t lo = 0, hi = 0;
-        if (valid) {
-            if (DENSE) { lo = j * d; hi = lo + d; }
-            else { lo = indptr[j]; hi = indptr[j + 1]; }
-        }
-        double dot = 0.0;
-        for (int64_t q = lo + gl; q < hi; q += G) {
-            const int r = DENSE ? (int)(q - lo) : rows[q];
-            dot += vals[q] * w[r];
-        }
-        dot = group_sum<G>(dot);
-        if (valid && gl == 0) {
+    for (int64_t cb = warp * 32; cb < n; cb += nwarps * 32) {
+        const double dot = warp_column_dots<G, DENSE>(cb, n, d, indptr, rows, vals, w);
+        const int64_t j = cb + lane;
+        if (j < n) {
             if (scores) scores[j] = dot;
             if (classify) {
                 const double p = sigmoid_tanh(dot);
@@ -294,10 +340,10 @@ int launch_gap(const glm_matrix *A, int kind, double lam, double rho, const doub
     const double avg = dense ? (double)A->n_rows
                              : (A->n_cols ? (double)A->nnz / (double)A->n_cols : 0.0);
 #define GAPL(G)                                                                               \
-    (dense ? gap_cols_kernel<G, true><<<RED_BLOCKS, RED_THREADS, 0, s>>>(                      \
+    (dense ? gap_cols_kernel<G, true><<<full_grid(gap_cols_kernel<G, true>), RED_THREADS, 0, s>>>( \
                  kind, lam, rho, y, A->n_cols, A->n_rows, A->indptr, A->rows, A->vals, alpha, \
                  w, out, scratch)                                                             \
-           : gap_cols_kernel<G, false><<<RED_BLOCKS, RED_THREADS, 0, s>>>(                     \
+           : gap_cols_kernel<G, false><<<full_grid(gap_cols_kernel<G, false>), RED_THREADS, 0, s>>>( \
                  kind, lam, rho, y, A->n_cols, A->n_rows, A->indptr, A->rows, A->vals, alpha, \
                  w, out, scratch))
     count_launch();
@@ -318,10 +364,10 @@ int launch_predict(const glm_matrix *X, const double *w, const double *y, int cl
     const double avg = dense ? (double)X->n_rows
                              : (X->n_cols ? (double)X->nnz / (double)X->n_cols : 0.0);
 #define PRL(G)                                                                                 \
-    (dense ? predict_kernel<G, true><<<RED_BLOCKS, RED_THREADS, 0, s>>>(                        \
+    (dense ? predict_kernel<G, true><<<full_grid(predict_kernel<G, true>), RED_THREADS, 0, s>>>( \
                  X->n_cols, X->n_rows, X->indptr, X->rows, X->vals, w, y, classify, scores,    \
                  prob, out, scratch)                                                           \
-           : predict_kernel<G, false><<<RED_BLOCKS, RED_THREADS, 0, s>>>(                       \
+           : predict_kernel<G, false><<<full_grid(predict_kernel<G, false>), RED_THREADS, 0, s>>>( \
                  X->n_cols, X->n_rows, X->indptr, X->rows, X->vals, w, y, classify, scores,    \
                  prob, out, scratch))
     count_launch();

@@ -308,12 +308,15 @@ class Engine:
             wk.gsum_ok = False
         self.stamp = 0
 
-    def capture(self, rounds):
+    def capture(self, rounds, on_round=None):
         """Record `rounds` outer rounds from the current state as one CUDA graph
         (requires sync_solves=False: no host round-trip inside a round; the
         NCCL all-reduce is captured too). Replay after reset():
         ``g = eng.capture(20); eng.reset(); g.replay()``. The graph's first
-        round computes G(0) from scratch, so call this right after reset()."""
+        round computes G(0) from scratch, so call this right after reset().
+        `on_round(r)` (optional) enqueues extra capture-safe work before the
+        first round (r = 0) and after round r = 1..rounds, e.g.
+        `gap_terms_async` into a per-round slot."""
         if self.sync_solves or self.chunk_runner is not None:
             raise ValueError("graph capture needs sync_solves=False and the device solver")
         D = _D()
@@ -327,8 +330,12 @@ class Engine:
         try:
             with torch.cuda.graph(graph, stream=side):
                 self.stream = torch.cuda.current_stream()
-                for _ in range(rounds):
+                if on_round is not None:
+                    on_round(0)
+                for r in range(rounds):
                     self.outer_round()
+                    if on_round is not None:
+                        on_round(r + 1)
                 for wk in self.workers.values():   # rejoin the prefetch branches
                     wk.solver.join(self.stream)
         finally:
@@ -534,6 +541,32 @@ class Engine:
                 raise SolverError("non-finite entries in shared view or coordinate update")
 
     # -- metrics ---------------------------------------------------------------
+    def gap_terms_async(self, out):
+        """Enqueue the fused gap kernels (+ the cross-rank sum of their partial
+        terms) into the 4-double device tensor `out` without a host round trip
+        (capture-safe): objective = out[3] + out[1], gap = out[0] + out[1] +
+        out[2] (engine.py:325-351)."""
+        self._flush_v()
+        D = _D()
+        a_local = self.alpha_dev[self.col_offset:self.col_offset + self.dm.n_cols]
+        ct = self._gap_coord_target()
+        L.check(L.lib().glm_gap_terms(
+            ctypes.byref(self.dm.struct), self.spec.index, self.spec.lam, self.spec.l1_ratio,
+            D.ptr(self.row_target), D.ptr(ct), D.ptr(a_local), D.ptr(self.v_dev),
+            D.ptr(self.w_scratch), D.ptr(out), D.ptr(D.scratch(self.stream)),
+            D.sptr(self.stream)), "glm_gap_terms")
+        if self.reducer is not None:                 # engine.py:339-341
+            self.reducer.allreduce_inplace(out[1:3])
+        return out
+
+    def _gap_coord_target(self):
+        if self.spec.coord_target is None:
+            return None
+        if getattr(self, "_gap_ct", None) is None:
+            self._gap_ct = _D().to_device(np.asarray(self.spec.coord_target)[
+                self.col_offset:self.col_offset + self.dm.n_cols])
+        return self._gap_ct
+
     def objective_and_gap(self):
         """(objective, gap) (engine.py:325-351) from the fused gap kernels."""
         self.check_solves()
