@@ -1,6 +1,7 @@
 """Summarise an ncu --set full report into profiles/<name>.json (+ print).
 
 usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/ncu_scd_async_c2.json [regex]
+traffic_bytes = DRAM read + write of the scd_async launch (else the first kernel).
 """
 import csv
 import io
@@ -44,7 +45,8 @@ for r in rows[2:]:
     kernels.append(rec)
 summary = {"report": rep, "kernels": kernels}
 if kernels:
-    k0 = kernels[0]
+    # traffic of the epoch kernel when the report has one (bench.py reads it)
+    k0 = next((k for k in kernels if "scd_async" in k["kernel"]), kernels[0])
     def to_bytes(key):
         v, u = k0.get(key), k0.get(key + ".unit", "byte")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
