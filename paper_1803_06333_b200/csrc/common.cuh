@@ -1,5 +1,6 @@
 // common.cuh — shared device code for the B200 GLM/TPA-SCD kernels (sm_100a).
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
@@ -265,6 +266,14 @@ void count_launch();
 // start (atomicMin) and latest end (atomicMax) of %globaltimer in slot pairs.
 enum { TL_EPOCH = 0, TL_PERM_FIRST = 1, TL_PERM_LAST = 2, TL_TURN = 3, TL_SCAN = 4, TL_SCATTER = 5,
        TL_SLOTS = 8 };
+// Programmatic dependent launch (kernels launched with launch_pdl): the
+// dependent grid is scheduled while this one drains; it waits for this grid's
+// completion and memory before touching its outputs.  No-ops otherwise.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ unsigned long long *d_timeline = nullptr;   // (one translation unit)
 __device__ __forceinline__ unsigned long long tl_now() {
     unsigned long long t;
@@ -284,6 +293,28 @@ __device__ __forceinline__ void tl_end_warp(int slot) {
     if (t && (threadIdx.x & 31) == 0) atomicMax(t + 2 * slot + 1, tl_now());
 }
 
+}  // namespace glm
+
+namespace glm {
+// <<<grid, block, smem, s>>> with the programmatic-stream-serialization
+// attribute when `pdl`: the kernel may be scheduled before its stream
+// predecessor has drained (it must call pdl_wait() before reading that
+// kernel's outputs).  Captured graphs keep it as a programmatic edge.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                              size_t smem, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 }  // namespace glm
 
 #define GLM_CUDA_TRY(expr)                                                   \

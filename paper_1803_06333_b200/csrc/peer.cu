@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     __shared__ uint32_t s_acc;
     SolveState *st = p.st;
     volatile SolveState *vst = st;
+    pdl_wait();                 // the epoch kernel's view, partials and state
     tl_start(TL_TURN);
     if (threadIdx.x == 0) {
         s_turn0 = vst->turn;
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         }
     }
     // ---- P3: every rank's Delta v, then the next round's start
+    pdl_trigger();              // the next epoch may be scheduled as blocks drain
     const int64_t R = s_R + 1;
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
@@ -725,8 +727,8 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
         if (rc) return rc;
     }
     count_launch();
-    round_turn_kernel<<<PEER_BLOCKS, TURN_THREADS, 0, st>>>(a);
-    GLM_CUDA_TRY(cudaGetLastError());
+    GLM_CUDA_TRY(launch_pdl(true, round_turn_kernel, dim3(PEER_BLOCKS), dim3(TURN_THREADS), 0, st,
+                            a));
     if (s->timing) return glue_end(s, st);
     return GLM_OK;
 }

@@ -66,6 +66,7 @@ struct EpochParams {
     int64_t nnz;
     int64_t seq;            // chunked mode: run only while chunk `seq` is open (-1: always)
     int reserve_blocks;     // async: block slots left free for the side-stream permutation
+    int pdl;                // async: launched as a programmatic dependent (turn rounds)
 };
 
 // A kernel of chunk `seq` runs only while that chunk is open and unfinished;
@@ -112,6 +113,7 @@ __device__ __forceinline__ void store_block_gsum(double g, double *gpart, SolveS
 template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
+    pdl_wait();
     if (skip_attempt(st, p.seq)) return;
     tl_start(TL_EPOCH);
     // CM bit 0: gather the view through L1 (ld.ca); bit 1: stream the column
@@ -212,6 +214,7 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
         }
     }
     store_block_gsum(gacc, p.gpart, st);
+    pdl_trigger();
     tl_end(TL_EPOCH);
 }
 
@@ -919,8 +922,8 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
     const int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
     count_launch();
-    scd_async<G, R, DENSE, CM><<<grid, 256, 0, s>>>(p);
-    GLM_CUDA_TRY(cudaGetLastError());
+    GLM_CUDA_TRY(launch_pdl(p.pdl != 0, scd_async<G, R, DENSE, CM>, dim3(grid), dim3(256), 0, s,
+                            p));
     return GLM_OK;
 }
 
@@ -1321,6 +1324,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     // GLM_FLAG_TURN: one attempt, and glm_round_turn follows on this stream
     const bool turn = (a->flags & GLM_FLAG_TURN) && a->max_attempts == 1 && a->epochs == 1 &&
                       m > 0;
+    ep.pdl = turn ? 1 : 0;        // the epoch follows the previous round's turn kernel
     const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
     auto ensure_side = [&]() -> int { return ensure_side_stream(s); };
     int launched = 0;
