@@ -104,8 +104,9 @@ __device__ __forceinline__ double group_sum(double v) {
 __device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
 
 // Block reduction of NV doubles (blockDim multiple of 32, <= 1024).
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* >= 32*NV */) {
+template <int NV, int NS>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (&smem)[NS]) {
+    static_assert(NS >= 32 * NV, "block_sum needs 32 shared doubles per value");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
 #pragma unroll

@@ -287,6 +287,66 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
 // independently of them and the grid is small (2 blocks per SM), so every
 // block becomes resident.  Replaces value + finalize + round start: three
 // kernel launches, ramps and tails per round become one.
+// decide_attempt (scd.cu) from state loaded up front: the fold's loads and
+// the state's loads share one round trip.  Returns 0 when the attempt was
+// rejected (the view goes back to the snapshot), else 1.
+constexpr int EPOCH_GPART_MAX = 16 * NUM_SMS;     // scd.cu EPOCH_PARTIALS
+struct DecideCache {
+    double value, damping, cnst;
+    int attempts, status, retries, dc, vw, epochs_run, epochs_target;
+};
+
+__device__ __forceinline__ void load_decide(volatile SolveState *st, const double *cnst,
+                                            DecideCache &c) {
+    c.value = st->value;
+    c.damping = st->damping;
+    c.cnst = *cnst;
+    c.attempts = st->attempts;
+    c.status = st->status;
+    c.retries = st->retries;
+    c.dc = st->dc;
+    c.vw = st->vw;
+    c.epochs_run = st->epochs_run;
+    c.epochs_target = st->epochs_target;
+}
+
+__device__ __forceinline__ int decide_cached(SolveState *st, const DecideCache &c, double G,
+                                             double gnew, double nonfinite) {
+    st->attempts = c.attempts + 1;
+    if (nonfinite > 0.0) {         // solver.py:279-280
+        st->status = GLM_SOLVER_ERROR;
+        st->done = 1;
+        return 1;
+    }
+    if (c.status != GLM_OK) {
+        st->done = 1;
+        return 1;
+    }
+    if (G > c.value) {
+        st->vw = c.vw ^ 1;
+        if (G - c.value <= PLATEAU_REL * (1.0 + fabs(c.value))) {
+            st->plateaued = 1;
+            st->done = 1;
+            return 0;
+        }
+        st->retries = c.retries + 1;
+        const double dmp = c.damping * 0.5;
+        st->damping = dmp;
+        if (dmp < DAMPING_FLOOR) {
+            st->status = GLM_DIVERGENCE;
+            st->done = 1;
+        }
+        return 0;
+    }
+    st->value = G;
+    st->gsum_acc = gnew;
+    st->dc = c.dc == 0 ? 1 : 0;
+    if (c.epochs_run < MAX_EPOCH_VALUES) st->epoch_values[c.epochs_run] = G;
+    st->epochs_run = c.epochs_run + 1;
+    if (c.epochs_run + 1 >= c.epochs_target) st->done = 1;
+    return 1;
+}
+
 struct TurnParams {
     SolveState *st;
     double *view0, *view1;
@@ -332,7 +392,7 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
 constexpr int TURN_THREADS = 512;
 
 __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) {
-    __shared__ double sm[96];
+    __shared__ double sm[32 * 4];      // block_sum<4>
     __shared__ int s_last;
     __shared__ uint32_t s_turn0;
     __shared__ int64_t s_R;
@@ -380,22 +440,34 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         if (s_last) {
             __threadfence();
             if (p.stamps && threadIdx.x == 0) p.stamps[7] = gtimer();
-            double tot[3] = {0.0, 0.0, 0.0};
+            // one round of independent loads: the decision's state (thread 0),
+            // the block partials and every possible epoch partial (masked by
+            // the epoch's grid size once it arrives) — the same sums, in the
+            // same order, as value_kernel mode 1 + decide_attempt
+            DecideCache dcache;
+            if (threadIdx.x == 0) load_decide(vst, p.cnst, dcache);
+            const int eb = active ? vst->epoch_blocks : 0;
+            double t4[4] = {0.0, 0.0, 0.0, 0.0};       // -, view terms, non-finite, g-sum
             for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-                tot[1] += __ldcg(p.partials + b * 3 + 1);
-                tot[2] += __ldcg(p.partials + b * 3 + 2);
+                t4[1] += __ldcg(p.partials + b * 3 + 1);
+                t4[2] += __ldcg(p.partials + b * 3 + 2);
             }
-            double gs[1] = {0.0};
-            if (active) {
-                const int eb = vst->epoch_blocks;
-                for (int b = threadIdx.x; b < eb; b += blockDim.x) gs[0] += __ldcg(p.gpart + b);
+            {
+                double gp[EPOCH_GPART_MAX / TURN_THREADS];
+#pragma unroll
+                for (int k = 0; k < EPOCH_GPART_MAX / TURN_THREADS; ++k)
+                    gp[k] = __ldcg(p.gpart + threadIdx.x + k * TURN_THREADS);
+#pragma unroll
+                for (int k = 0; k < EPOCH_GPART_MAX / TURN_THREADS; ++k)
+                    if ((int)threadIdx.x + k * TURN_THREADS < eb) t4[3] += gp[k];
             }
-            block_sum<3>(tot, sm);
-            block_sum<1>(gs, sm);
+            block_sum<4>(t4, sm);
             if (threadIdx.x == 0) {
                 st->block_counter = 0;
-                if (active) decide_attempt(st, *p.cnst + tot[1] / p.quad + gs[0], gs[0], tot[2], 0);
-                const int accept = st->vw == vw0;
+                int accept = 1;
+                if (active)
+                    accept = decide_cached(st, dcache, dcache.cnst + t4[1] / p.quad + t4[3], t4[3],
+                                           t4[2]);
                 __threadfence();
                 if (p.stamps) p.stamps[1] = gtimer();
                 atomicAdd(&st->turn, 1u);          // the other blocks go on to alpha
