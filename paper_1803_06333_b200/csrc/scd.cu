@@ -65,7 +65,6 @@ struct EpochParams {
     double *gpart;          // per-block partial sum_j g(base_j + delta_j) of the epoch
     int64_t nnz;
     int64_t seq;            // chunked mode: run only while chunk `seq` is open (-1: always)
-    int reserve_blocks;     // async: block slots left free for the side-stream permutation
     int pdl;                // async: launched as a programmatic dependent (turn rounds)
 };
 
@@ -917,7 +916,7 @@ static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s
     if (groups > p.m) groups = p.m;
     if (groups < 32 / G) groups = 32 / G;
     const int64_t need_blocks = (groups * G + 255) / 256;
-    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS - p.reserve_blocks;
+    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
     if (cap < NUM_SMS) cap = NUM_SMS;
     if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
     const int grid = (int)(need_blocks < cap ? (need_blocks < 1 ? 1 : need_blocks) : cap);
@@ -1313,7 +1312,6 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     int32_t *P = s->perm_cur ? s->perm_b : s->perm;
     int32_t *P_alt = s->perm_cur ? s->perm : s->perm_b;
     ep.perm = P;
-    ep.reserve_blocks = 0;
     // Early prefetch: with one attempt per solve the generator advances by
     // exactly m keys, so the host knows the next solve's start state and its
     // permutation can be generated on the side stream into the other buffer
