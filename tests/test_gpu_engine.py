@@ -128,3 +128,31 @@ def test_async_engine_reaches_gap_target():
         rounds[mode] = res.rounds
     print("epochs to target", rounds)
     assert abs(rounds["async"] - rounds["sequential"]) <= max(1, 0.1 * rounds["sequential"])
+
+
+def test_turn_rejected_attempt_leaves_alpha_and_v():
+    """A rejected attempt in the fused round turn (one attempt per round): the
+    view goes back to the snapshot, so Delta v is exactly zero and the flag's
+    accept bit makes every rank add +0.0 (peer.cu publish/rank_sum); alpha
+    and v stay bit-identical (solver.py:281-290).  512 identical columns
+    updated concurrently from a stale view overshoot by ~512x."""
+    rng = np.random.default_rng(4)
+    d, n = 8, 512
+    col = rng.standard_normal(d)
+    m = g.SparseColumnMatrix(d, np.arange(0, n * d + 1, d),
+                             np.tile(np.arange(d, dtype=np.int32), n), np.tile(col, n),
+                             validate=False)
+    spec = g.ObjectiveSpec("ridge_primal", 1e-3, d, n, target=rng.standard_normal(d))
+    eng = g.Engine(m, spec, g.HierarchyConfig(t1=10, seed=0, epochs=1), mode="async",
+                   sync_solves=False, retry_budget=0, max_inflight=4096)
+    assert eng.exchange is not None
+    a0, v0 = eng.alpha.copy(), eng.v.copy()
+    eng.outer_round()
+    # (the turn already reset the solver state for the next round, so the
+    # rejection shows as an unchanged alpha: every coordinate's step is nonzero)
+    assert eng.alpha.tobytes() == a0.tobytes()
+    assert eng.v.tobytes() == v0.tobytes()
+    seq = g.Engine(m, spec, g.HierarchyConfig(t1=10, seed=0, epochs=1), mode="sequential",
+                   sync_solves=False, retry_budget=0)
+    seq.outer_round()
+    assert np.any(seq.alpha != a0) and np.any(seq.v != v0)   # an accepted pass moves both
