@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
 // rejected (the view goes back to the snapshot), else 1.
 constexpr int EPOCH_GPART_MAX = 16 * NUM_SMS;     // scd.cu EPOCH_PARTIALS
 struct DecideCache {
-    double value, damping, cnst;
+    double value, damping, cnst, gsum;
     int attempts, status, retries, dc, vw, epochs_run, epochs_target;
 };
 
@@ -301,6 +301,7 @@ __device__ __forceinline__ void load_decide(volatile SolveState *st, const doubl
     c.value = st->value;
     c.damping = st->damping;
     c.cnst = *cnst;
+    c.gsum = st->gsum_acc;
     c.attempts = st->attempts;
     c.status = st->status;
     c.retries = st->retries;
@@ -416,14 +417,27 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     // exchange buffer on the same pass (the loads are shared).  If the attempt
     // is rejected the view reverts to the snapshot, which is lin, so the true
     // Delta v is exactly zero: the accept word tells the peers to add +0.0.
+    // The same pass sums f(v) for the round's constant: v has not changed
+    // since the previous turn's P3 (which therefore skips that reduction), so
+    // const = f(v)/K/L and G(0) = const + g-sum are formed here, where the
+    // decision needs them.
     {
         const int vw0 = vst->vw;
         const double *V = vw0 ? p.view1 : p.view0;
-        double acc[3] = {0.0, 0.0, 0.0};
+        const bool dual = kind_is_dual(p.kind);
+        double acc[3] = {0.0, 0.0, 0.0};           // f(v), view terms, non-finite
         for (int64_t r = tid; r < p.d; r += nth) {
-            const double x = __ldcg(V + r), l = p.lin[r];
+            const double x = __ldcg(V + r), l = p.lin[r], vr = p.v[r];
             const double u = x - l;
             out[r] = u / p.quad;
+            double f, g;                            // outer_model_kernel's arithmetic
+            if (dual) {
+                f = vr * vr;
+            } else {
+                f_terms(p.kind, p.lam, p.tgt[r], vr, f, g);
+                if (p.kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;
+            }
+            acc[0] += f;
             if (active) {
                 if (!isfinite(x)) acc[2] += 1.0;
                 acc[1] += l * u + 0.5 * u * u;
@@ -431,6 +445,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         }
         block_sum<3>(acc, sm);
         if (threadIdx.x == 0) {
+            p.partials[blockIdx.x * 3 + 0] = acc[0];
             p.partials[blockIdx.x * 3 + 1] = acc[1];
             p.partials[blockIdx.x * 3 + 2] = acc[2];
             __threadfence();        // partials and Delta v before the arrival
@@ -447,8 +462,9 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             DecideCache dcache;
             if (threadIdx.x == 0) load_decide(vst, p.cnst, dcache);
             const int eb = active ? vst->epoch_blocks : 0;
-            double t4[4] = {0.0, 0.0, 0.0, 0.0};       // -, view terms, non-finite, g-sum
+            double t4[4] = {0.0, 0.0, 0.0, 0.0};       // f(v), view terms, non-finite, g-sum
             for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+                t4[0] += __ldcg(p.partials + b * 3 + 0);
                 t4[1] += __ldcg(p.partials + b * 3 + 1);
                 t4[2] += __ldcg(p.partials + b * 3 + 2);
             }
@@ -464,10 +480,20 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             block_sum<4>(t4, sm);
             if (threadIdx.x == 0) {
                 st->block_counter = 0;
+                double f = t4[0];                       // round_start_kernel's scaling
+                if (kind_is_dual(p.kind)) f = f / (2.0 * p.lam);
+                else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+                const double cn = (f / p.K + 0.0) / p.L;
+                *p.out_fv = f;
+                *p.cnst = cn;
                 int accept = 1;
-                if (active)
-                    accept = decide_cached(st, dcache, dcache.cnst + t4[1] / p.quad + t4[3], t4[3],
-                                           t4[2]);
+                if (active) {
+                    dcache.cnst = cn;
+                    dcache.value = cn + dcache.gsum;    // G(0): begin_kernel with reuse_gsum
+                    st->value = dcache.value;
+                    st->initial = dcache.value;
+                    accept = decide_cached(st, dcache, cn + t4[1] / p.quad + t4[3], t4[3], t4[2]);
+                }
                 __threadfence();
                 if (p.stamps) p.stamps[1] = gtimer();
                 atomicAdd(&st->turn, 1u);          // the other blocks go on to alpha
@@ -478,6 +504,8 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         if (threadIdx.x == 0) {
             while (ld_acquire_gpu_u32(&st->turn) == s_turn0) __nanosleep(32);
             s_dc = vst->dc;
+            // read: block 0 may now reset the solver state (end of P3)
+            atomicAdd(&st->block_counter, 1u);
         }
         __syncthreads();
     }
@@ -531,7 +559,6 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     __syncthreads();
     const int64_t off = (R & 1) * p.pstride;
     const uint32_t accm = s_acc;
-    double acc[1] = {0.0};
     const bool dual = kind_is_dual(p.kind);
     for (int64_t r = tid; r < p.d; r += nth) {
         const double s = rank_sum(p.bufs, p.world, off + r, accm);
@@ -539,33 +566,25 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         p.v[r] = x;
         double f, g;
         if (dual) {
-            f = x * x;
             g = x / p.lam;
         } else {
             f_terms(p.kind, p.lam, p.tgt[r], x, f, g);
-            if (p.kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;
         }
-        acc[0] += f;
         p.grad[r] = g;
         p.lin[r] = g;
         p.view0[r] = g;
         p.view1[r] = g;
     }
-    if (!reduce_last<1>(acc, p.scratch)) return;
+    // f(v), the constant and G(0) of the next round are formed by its P1;
+    // block 0 resets the solver state once every block has read the decision
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    while (ld_acquire_gpu_u32(&st->block_counter) < gridDim.x) __nanosleep(32);
+    st->block_counter = 0;
     tl_end(TL_TURN);
-    double f = acc[0];
-    if (dual) f = f / (2.0 * p.lam);
-    else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
-    *p.out_fv = f;
-    const double cn = (f / p.K + 0.0) / p.L;
-    *p.cnst = cn;
     p.ctl[1] = R;
     if (p.stamps) p.stamps[4] = gtimer();
     if (st->status != GLM_OK) return;          // keep a solver error visible to the host
-    const double G0 = cn + st->gsum_acc;       // begin_kernel with reuse_gsum, reset damping
-    st->value = G0;
-    st->initial = G0;
-    st->gen_state = st->gen_next;
+    st->gen_state = st->gen_next;              // begin_kernel with reuse_gsum, reset damping
     st->damping = 1.0;
     st->epochs_target = p.epochs;
     st->epochs_run = 0;
