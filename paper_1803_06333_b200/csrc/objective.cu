@@ -181,25 +181,25 @@ __global__ void __launch_bounds__(RED_THREADS) gap_rows_kernel(int kind, double 
 }
 
 // a_j.w by the G lanes of a column group: each lane takes every G-th entry;
-// four entries per lane are loaded (indices, values, then the gathers) before
+// U entries per lane are loaded (indices, values, then the gathers) before
 // any is added, in the same order as a plain strided loop.
-template <int G, bool DENSE>
+template <int G, bool DENSE, int U = 4>
 __device__ __forceinline__ double column_dot(int64_t lo, int64_t hi, int gl, const int32_t *rows,
                                              const double *vals, const double *w) {
     double dot = 0.0;
-    for (int64_t q0 = lo + gl; q0 < hi; q0 += 4 * G) {
-        int r[4];
-        double a[4], x[4];
+    for (int64_t q0 = lo + gl; q0 < hi; q0 += U * G) {
+        int r[U];
+        double a[U], x[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int64_t q = q0 + (int64_t)u * G;
             r[u] = q < hi ? (DENSE ? (int)(q - lo) : __ldg(rows + q)) : -1;
             a[u] = q < hi ? __ldg(vals + q) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = r[u] >= 0 ? w[r[u]] : 0.0;
+        for (int u = 0; u < U; ++u) x[u] = r[u] >= 0 ? w[r[u]] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < U; ++u)
             if (r[u] >= 0) dot += a[u] * x[u];
     }
     return group_sum<G>(dot);
@@ -210,7 +210,7 @@ __device__ __forceinline__ double column_dot(int64_t lo, int64_t hi, int gl, con
 // (bounds handed over by shuffles, no dependent indptr load per column), and
 // every dot lands in the lane of its column, so the per-column epilogue
 // (transcendentals, loads of alpha / labels) runs on all 32 lanes.
-template <int G, bool DENSE>
+template <int G, bool DENSE, int U = 4>
 __device__ __forceinline__ double warp_column_dots(int64_t cb, int64_t n, int64_t d,
                                                    const int64_t *indptr, const int32_t *rows,
                                                    const double *vals, const double *w) {
@@ -228,7 +228,7 @@ __device__ __forceinline__ double warp_column_dots(int64_t cb, int64_t n, int64_
         const int src = it * GPW + sub;
         const int64_t lo = __shfl_sync(0xffffffffu, mlo, src);
         const int64_t hi = __shfl_sync(0xffffffffu, mhi, src);
-        const double dot = column_dot<G, DENSE>(lo, hi, gl, rows, vals, w);
+        const double dot = column_dot<G, DENSE, U>(lo, hi, gl, rows, vals, w);
         const double v = __shfl_sync(0xffffffffu, dot, (lane % GPW) * G);
         if (lane / GPW == it) mine = v;
     }
@@ -236,7 +236,7 @@ __device__ __forceinline__ double warp_column_dots(int64_t cb, int64_t n, int64_
 }
 
 // gap part B over the columns: s_j = -a_j.w; g(alpha_j) + g*(s_j)
-template <int G, bool DENSE>
+template <int G, bool DENSE, int U = 4>
 __global__ void __launch_bounds__(RED_THREADS) gap_cols_kernel(
     int kind, double lam, double rho, const double *y, int64_t n, int64_t d,
     const int64_t *indptr, const int32_t *rows, const double *vals, const double *alpha,
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(RED_THREADS) gap_cols_kernel(
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t cb = warp * 32; cb < n; cb += nwarps * 32) {
-        const double dot = warp_column_dots<G, DENSE>(cb, n, d, indptr, rows, vals, w);
+        const double dot = warp_column_dots<G, DENSE, U>(cb, n, d, indptr, rows, vals, w);
         const int64_t j = cb + lane;
         if (j < n) {
             const double yj = y ? y[j] : 0.0;
@@ -347,11 +347,19 @@ int launch_gap(const glm_matrix *A, int kind, double lam, double rho, const doub
                  kind, lam, rho, y, A->n_cols, A->n_rows, A->indptr, A->rows, A->vals, alpha, \
                  w, out, scratch))
     count_launch();
-    switch (pick_lanes(avg)) {
-    case 4: GAPL(4); break;
-    case 8: GAPL(8); break;
-    case 16: GAPL(16); break;
-    default: GAPL(32); break;
+    if (!dense && avg > 12 && avg <= 48) {
+        // ~40-nnz columns (C2, C5): 4 lanes x 12 entries each, so a warp has
+        // 8 columns' gathers in flight at once instead of 2
+        gap_cols_kernel<4, false, 12><<<full_grid(gap_cols_kernel<4, false, 12>), RED_THREADS, 0,
+                                        s>>>(kind, lam, rho, y, A->n_cols, A->n_rows, A->indptr,
+                                             A->rows, A->vals, alpha, w, out, scratch);
+    } else {
+        switch (pick_lanes(avg)) {
+        case 4: GAPL(4); break;
+        case 8: GAPL(8); break;
+        case 16: GAPL(16); break;
+        default: GAPL(32); break;
+        }
     }
 #undef GAPL
     GLM_CUDA_TRY(cudaGetLastError());

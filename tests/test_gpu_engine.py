@@ -156,3 +156,17 @@ def test_turn_rejected_attempt_leaves_alpha_and_v():
                    sync_solves=False, retry_budget=0)
     seq.outer_round()
     assert np.any(seq.alpha != a0) and np.any(seq.v != v0)   # an accepted pass moves both
+
+
+def test_gap_matches_oracle_on_c2_shape():
+    """The fused gap kernels on 40-nnz columns (the wide-chunk column pass)
+    against the oracle's duality gap (engine.py:325-351, objectives.py:205-234)."""
+    m = _c2_like(30_000, 3_000, 40, 11)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
+    eng = g.Engine(m, spec, g.HierarchyConfig(t1=3, seed=2, epochs=1))
+    for _ in range(2):
+        obj, gap = eng.objective_and_gap()
+        om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+        want = oracle.duality_gap("dual_l2_logistic", 1.0, om, eng.alpha, eng.v)
+        assert gap == pytest.approx(want, rel=1e-9, abs=1e-9 * abs(obj))
+        eng.outer_round()
