@@ -17,7 +17,8 @@ eng = g.Engine(dm, spec, g.HierarchyConfig(t1=10**6, seed=0, epochs=1), mode="as
 for _ in range(3):
     eng.outer_round()
 eng.reset()
-graph = eng.capture(1)            # one fused round per replay
+ROUNDS = int(os.environ.get("TL_ROUNDS", "1"))
+graph = eng.capture(ROUNDS)       # ROUNDS fused rounds per replay (stamps: first start, last end)
 slots = torch.zeros(16, dtype=torch.int64, device="cuda")
 init = torch.tensor([2**63 - 1, 0] * 8, dtype=torch.int64, device="cuda")
 L.check(L.lib().glm_debug_timeline(slots.data_ptr()), "timeline")
@@ -38,3 +39,9 @@ names = ["epoch start", "epoch end", "perm first start", "perm first end", "perm
          "perm scatter start", "perm scatter end"]
 for n, v in zip(names, med):
     print(f"{n:18s} {v:9.2f} us")
+if ROUNDS > 1:
+    span = med[1] - med[0]
+    print(f"{ROUNDS} rounds: first epoch start -> last epoch end {span:.1f} us, "
+          f"{span / ROUNDS:.1f} us per round (epoch end -> turn end of the last round "
+          f"{med[7] - med[1]:.1f} us)")
+
