@@ -7,8 +7,9 @@
 // model (engine.py:271-272, 242-250, 148-166) and solve start (solver.py:
 // 268-270).  Here:
 //
-//   finalize (rank r):  alpha += delta; dv_r[b] = B delta; publish: flag slot r
-//                       of every rank = R+1 (release, system scope, NVLink store)
+//   finalize (rank r):  alpha += delta; dv_r[b] = B delta; publish: one
+//                       system-scope fence, then the flag word (R+1, accept
+//                       bits) stored into slot r of every rank's flags
 //   round start:        wait until every LOCAL flag slot j >= R (acquire,
 //                       system scope; no remote round trip per poll);
 //                       v += sum_j dv_j[b] in ascending rank order (the bits of
@@ -36,7 +37,7 @@ struct glm_peer {
     int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter,
                                   // [3] "every rank published" (turn), [4] their accept
                                   // bits, [5] our last flag word
-    int64_t *flags = nullptr;     // local slots: flags[j] = last round rank j published
+    int64_t *flags = nullptr;     // local slots: flags[j] = rank j's last flag word
     double *dv = nullptr;         // 2 halves of pstride doubles (Delta v[d], padded)
     int64_t pstride = 0;
     double **bufs_dev = nullptr;  // world pointers to each rank's dv (device array)
