@@ -585,9 +585,15 @@ def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world
 
     lin, base, dl, dvb = pinned(d), pinned(m), pinned(m), pinned(d)
     base[:] = 0.5
-    v0 = np.zeros(d)
+    # the first round's subproblem from alpha0 = 0.5 (engine.py:131-166,
+    # 211-212): v0 = A alpha0 over every rank's examples, lin = f'(v0) = v0/lambda,
+    # quad = sigma/lambda, const = f(v0)/K
+    v0 = np.bincount(rows, weights=0.5 * np.asarray(vals), minlength=d).astype(np.float64)
+    if reducer is not None:
+        v0 = np.asarray(reducer.allreduce_sum(v0), dtype=np.float64)
     lin[:] = v0 / LAM
-    sub = g.LocalSubproblem(spec=spec, lin=lin, quad=world / LAM, const=0.0, base=base,
+    sub = g.LocalSubproblem(spec=spec, lin=lin, quad=world / LAM,
+                            const=float(v0 @ v0) / (2.0 * LAM) / world, base=base,
                             data=None, col_ids=np.arange(m))
     gen_state = g.derive_seed(0, 0)
     damping = 1.0

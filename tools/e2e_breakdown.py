@@ -39,9 +39,11 @@ _lib.check(_lib.lib().glm_ctx_create(0, _lib.CSC, d, m, indptr.ctypes.data_as(ct
 pin = lambda n: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
 lin, base, dl, dvb = pin(d), pin(m), pin(m), pin(d)
 base[:] = 0.5
-lin[:] = 0.0
-spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, bench.N_EX, bench.D_FEAT)
-sub = g.LocalSubproblem(spec=spec, lin=lin, quad=1.0, const=0.0, base=base, data=None,
+v0 = np.bincount(rows, weights=0.5 * vals, minlength=d)      # first round: v0 = A alpha0
+lin[:] = v0 / bench.LAM
+spec = g.ObjectiveSpec("dual_l2_logistic", bench.LAM, bench.N_EX, bench.D_FEAT)
+sub = g.LocalSubproblem(spec=spec, lin=lin, quad=1.0 / bench.LAM,
+                        const=float(v0 @ v0) / (2.0 * bench.LAM), base=base, data=None,
                         col_ids=np.arange(m))
 st = g.derive_seed(0, 0)
 print("plugin_call_ms", round(med(lambda: device_solve_host(h, sub, st, 1.0, 1, 1, out=(dl, dvb))), 4))
