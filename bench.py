@@ -448,6 +448,7 @@ def ours_main(args):
     phase("e2e done", rank)
     # -------- time to 1e-3 suboptimality (certified by the duality gap)
     ttt = None
+    eng2 = None
     if not args.no_ttt:
         eng2 = make_engine()
         torch.cuda.synchronize()
@@ -505,13 +506,21 @@ def ours_main(args):
                                  "epochs_run_last_round": int(res_state.epochs_run),
                                  "damping": float(res_state.damping)}}
         print(json.dumps(line), flush=True)
-    # Every collective of this run has completed (the JSON line needed them all).
-    # Leave without the NCCL teardown: destroying a communicator that CUDA
-    # graphs captured can block the watchdog past the driver's limits.
+    # Normal interpreter exit (atexit hooks run): drop the captured graphs and
+    # engines first, then tear the process group down on every rank together.
+    del graph, graph_inst
     torch.cuda.synchronize()
+    for e in (eng, eng2):
+        if e is not None:
+            e.close()
+    del eng, eng2
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
     sys.stdout.flush()
     sys.stderr.flush()
-    os._exit(0)
+    return 0
 
 
 def ttt_graph(eng, rounds, world):

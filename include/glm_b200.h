@@ -384,6 +384,15 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
                     double *out_fv, double *cnst, double n_nodes, double n_devices, int epochs,
                     double *scratch, void *stream);
 int glm_peer_destroy(glm_peer *p);
+/* Deadline of every device-side wait of the exchange (default 60 s, the
+ * reference's DEFAULT_TIMEOUT, comm.py:30).  A wait that expires records
+ * itself in the exchange's error word and lets its kernel finish. */
+int glm_peer_set_timeout(glm_peer *p, double seconds);
+/* Synchronises the device and reads the error word: 0 = none, else
+ * (kind << 32 | what): kind 1 = rank `what` did not publish in time (a dead or
+ * stalled peer, -> ReduceError), kind 2 = the turn's grid was not co-resident.
+ * clear != 0 resets it. */
+int glm_peer_error(glm_peer *p, int64_t *code_out, int clear);
 /* Debug: glm_round_turn writes %globaltimer stamps (ns) of its phases into
  * device u64[8]: start, decided, published, every rank seen, done (NULL: off). */
 int glm_peer_stamps(glm_peer *p, uint64_t *device_array);

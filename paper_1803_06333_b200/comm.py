@@ -118,6 +118,9 @@ class NcclReducer:
         self.device = device if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if self.on_cuda
             else torch.device("cpu"))
+        # gloo: device tensors are staged through host memory (several ranks
+        # may then share one GPU, which NCCL refuses)
+        self.staged = not self.on_cuda
         self._aborted = False
 
     def handshake(self):
@@ -146,10 +149,19 @@ class NcclReducer:
             hi, neg_lo = n.tolist()
             if hi != -neg_lo:
                 raise ProtocolError("vector length mismatch")
-        if self.deterministic:
+        if self.deterministic and self.staged:
+            h = t.cpu()
+            got = [torch.empty_like(h) for _ in range(self.world)]
+            dist.all_gather(got, h, group=self.group)
+            res = canonical_sum(got).to(t.device)                  # ascending rank order
+        elif self.deterministic:
             flat = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
             dist.all_gather_into_tensor(flat, t, group=self.group)
             res = canonical_sum(list(flat.view(self.world, -1)))   # ascending rank order
+        elif self.staged and t.is_cuda:
+            res = t.cpu()
+            dist.all_reduce(res, op=dist.ReduceOp.SUM, group=self.group)
+            res = res.to(t.device)
         else:
             res = t.clone()
             dist.all_reduce(res, op=dist.ReduceOp.SUM, group=self.group)
@@ -159,12 +171,18 @@ class NcclReducer:
             else:
                 out.copy_(res)
             return out
-        return res if was_tensor else res.cpu().numpy()
+        return res.to(vec.device) if was_tensor else res.cpu().numpy()
 
     def allreduce_inplace(self, t):
         """Fast path for device-resident engines: sum into `t` (NCCL)."""
+        if self._aborted:
+            raise ReduceError("collective aborted")
         if self.deterministic:
             t.copy_(self.allreduce_sum(t))
+        elif self.staged and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
         else:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
@@ -201,34 +219,79 @@ class PeerExchange:
     every rank's Delta v stays in its own HBM, mapped into every peer with
     CUDA IPC; `glm_round_start` sums the ranks' buffers in ascending rank order
     (the bits of canonical_sum on every rank, comm.py:41-46) fused with
-    v += total and the next round's model. World 1 works without IPC."""
+    v += total and the next round's model. World 1 works without IPC.
 
-    def __init__(self, d, group=None, local=False):
+    Construction is collective and agreed: every rank joins both exchanges
+    (handles, then the open results) even after a local failure, and if any
+    rank failed every rank closes and raises ReduceError — so all ranks fall
+    back to the NCCL path together.  Every device-side wait has a deadline
+    (`timeout`, default the reference's DEFAULT_TIMEOUT = 60 s, comm.py:30);
+    `check()` raises ReduceError when one expired (a dead or stalled peer)."""
+
+    DEFAULT_TIMEOUT = 60.0
+
+    def __init__(self, d, group=None, local=False, timeout=None):
         import ctypes
 
         from . import _lib as L
         self.L = L
+        self.handle = None
         multi = dist.is_initialized() and not local
         self.world = dist.get_world_size(group) if multi else 1
         self.rank = dist.get_rank(group) if multi else 0
         self.d = int(d)
+        self.timeout = float(self.DEFAULT_TIMEOUT if timeout is None else timeout)
         h = ctypes.c_void_p()
-        L.check(L.lib().glm_peer_create(torch.cuda.current_device(), self.d, self.rank,
-                                        self.world, ctypes.byref(h)), "glm_peer_create")
-        self.handle = h
+        err = None
+        mine = b""
+        try:
+            L.check(L.lib().glm_peer_create(torch.cuda.current_device(), self.d, self.rank,
+                                            self.world, ctypes.byref(h)), "glm_peer_create")
+            self.handle = h
+            L.check(L.lib().glm_peer_set_timeout(h, self.timeout), "glm_peer_set_timeout")
+            if self.world > 1:
+                nb = int(L.lib().glm_peer_handle_bytes())
+                buf = (ctypes.c_char * nb)()
+                L.check(L.lib().glm_peer_handle(h, buf), "glm_peer_handle")
+                mine = bytes(buf)
+        except Exception as exc:          # still join the collectives below
+            err = exc
         if self.world > 1:
-            nb = int(L.lib().glm_peer_handle_bytes())
-            mine = (ctypes.c_char * nb)()
-            L.check(L.lib().glm_peer_handle(h, mine), "glm_peer_handle")
             got = [None] * self.world
-            dist.all_gather_object(got, bytes(mine), group=group)
-            blob = b"".join(got)
-            try:
-                L.check(L.lib().glm_peer_open(h, ctypes.c_char_p(blob)), "glm_peer_open")
-            except Exception:
-                L.lib().glm_peer_destroy(h)
-                self.handle = None
-                raise
+            dist.all_gather_object(got, (err is None, mine), group=group)
+            if err is None and not all(ok for ok, _ in got):
+                err = ReduceError("peer exchange: another rank could not create its buffers")
+            if err is None:
+                try:
+                    L.check(L.lib().glm_peer_open(h, ctypes.c_char_p(b"".join(b for _, b in got))),
+                            "glm_peer_open")
+                except Exception as exc:
+                    err = exc
+            oks = [None] * self.world
+            dist.all_gather_object(oks, err is None, group=group)
+            if err is None and not all(oks):
+                err = ReduceError("peer exchange: another rank could not map the buffers")
+        if err is not None:
+            self.close()
+            if isinstance(err, ReduceError):
+                raise err
+            raise ReduceError(f"peer exchange unavailable: {err}") from err
+
+    def check(self):
+        """Raise ReduceError if a device-side wait ran past the deadline
+        (synchronises the device)."""
+        import ctypes
+        code = ctypes.c_int64(0)
+        self.L.check(self.L.lib().glm_peer_error(self.handle, ctypes.byref(code), 0),
+                     "glm_peer_error")
+        c = code.value
+        if c:
+            kind, what = c >> 32, c & 0xFFFFFFFF
+            if kind == 1:
+                raise ReduceError(f"peer exchange: rank {what} did not publish its Delta v "
+                                  f"within {self.timeout:g} s (dead or stalled peer)")
+            raise ReduceError(f"peer exchange: round_turn blocks were not co-resident "
+                              f"(wait {what} expired after {self.timeout:g} s)")
 
     def consume(self, stream):
         from . import _device as D
@@ -245,3 +308,17 @@ class PeerExchange:
             self.close()
         except Exception:
             pass
+
+
+def shutdown(*engines):
+    """Orderly end of a (multi-process) run: close the engines' peer exchanges,
+    synchronise, and tear the process group down on every rank together, so
+    the interpreter exits normally (atexit hooks run)."""
+    for eng in engines:
+        if eng is not None and hasattr(eng, "close"):
+            eng.close()
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.synchronize()
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()

@@ -36,7 +36,8 @@ struct glm_peer {
     char *mem = nullptr;
     int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter,
                                   // [3] "every rank published" (turn), [4] their accept
-                                  // bits, [5] our last flag word
+                                  // bits, [5] our last flag word, [6] round-start ticket,
+                                  // [7] error word (a wait that timed out)
     int64_t *flags = nullptr;     // local slots: flags[j] = rank j's last flag word
     double *dv = nullptr;         // 2 halves of pstride doubles (Delta v[d], padded)
     int64_t pstride = 0;
@@ -44,6 +45,8 @@ struct glm_peer {
     int64_t **flags_dev = nullptr;  // world pointers to each rank's flag slots
     std::vector<void *> opened;   // cudaIpc-opened peer allocations
     uint64_t *stamps = nullptr;   // glm_peer_stamps: turn phase timestamps (debug)
+    uint64_t timeout_ns = 60000000000ull;   // every device-side wait (comm.py:30 DEFAULT_TIMEOUT)
+    int turn_blocks = 0;          // co-resident grid of round_turn (occupancy-checked)
     cudaIpcMemHandle_t handle{};
 };
 
@@ -103,14 +106,43 @@ __device__ __forceinline__ void publish(int64_t *ctl, int64_t *const *flags, int
     }
 }
 
+// Error word ctl[7] (read by glm_peer_error): the first wait that ran past
+// the deadline records what it waited for; the kernel then runs to its end
+// (a missing rank contributes +0.0) so the host can raise instead of hanging.
+enum : int64_t { PEER_ERR_FLAGS = 1, PEER_ERR_GRID = 2 };
+
+__device__ __forceinline__ void peer_fail(int64_t *ctl, int64_t code, int64_t what) {
+    atomicCAS(reinterpret_cast<unsigned long long *>(ctl + 7), 0ull,
+              (unsigned long long)((code << 32) | (what & 0xffffffff)));
+}
+
+// A spin with a %globaltimer deadline: true once `timeout` ns have passed
+// since t0 (t0 = 0 starts the clock).
+__device__ __forceinline__ bool expired(uint64_t &t0, uint64_t timeout) {
+    const uint64_t t = gtimer();
+    if (t0 == 0) t0 = t;
+    return t - t0 > timeout;
+}
+
 // Every local flag slot at round >= R (one thread); returns the ranks'
-// accept bits of round R.
-__device__ __forceinline__ uint32_t wait_flags(const int64_t *flags, int world, int64_t R) {
+// accept bits of round R.  A rank that has not published within the deadline
+// is recorded in ctl[7] and counted as not accepted (its Delta v is skipped).
+__device__ __forceinline__ uint32_t wait_flags(const int64_t *flags, int world, int64_t R,
+                                               int64_t *ctl, uint64_t timeout) {
     uint32_t mask = 0;
+    uint64_t t0 = 0;
     for (int j = 0; j < world; ++j) {
         int64_t f;
-        while (((f = ld_acquire_sys(flags + j)) >> 2) < R) __nanosleep(32);
-        mask |= (uint32_t)((f >> (R & 1)) & 1) << j;
+        bool late = false;
+        while (((f = ld_acquire_sys(flags + j)) >> 2) < R) {
+            __nanosleep(32);
+            if (expired(t0, timeout)) {
+                peer_fail(ctl, PEER_ERR_FLAGS, j);
+                late = true;
+                break;
+            }
+        }
+        if (!late) mask |= (uint32_t)((f >> (R & 1)) & 1) << j;
     }
     return mask;
 }
@@ -197,6 +229,7 @@ struct RoundStart {
     double *view0, *view1;
     int epochs;
     double *scratch;
+    uint64_t timeout;
 };
 
 __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p) {
@@ -207,7 +240,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
         const int64_t R = p.ctl[0], C = p.ctl[1];
         s_R = R;
         s_apply = R > C;
-        s_acc = R > C ? wait_flags(p.flags, p.world, R) : 0u;
+        s_acc = R > C ? wait_flags(p.flags, p.world, R, p.ctl, p.timeout) : 0u;
     }
     __syncthreads();
     const int apply = s_apply;
@@ -241,7 +274,19 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
         }
     }
     if (p.mode == 0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && apply) p.ctl[1] = s_R;
+        // consumed = R only after every block has read (ctl[0], ctl[1]) and made
+        // its apply decision: the last block to arrive on the ticket ctl[6]
+        // writes it (a block scheduled late must still see C < R)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned long long t =
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl + 6), 1ull);
+            if (t == (unsigned long long)(gridDim.x - 1)) {
+                p.ctl[6] = 0;
+                if (apply) p.ctl[1] = s_R;
+            }
+        }
         return;
     }
     if (!reduce_last<1>(acc, p.scratch)) return;
@@ -376,6 +421,7 @@ struct TurnParams {
     int epochs;
     double *scratch;
     uint64_t *stamps;          // optional phase timestamps (globaltimer ns)
+    uint64_t timeout;          // deadline of every wait (ns)
 };
 
 
@@ -503,7 +549,14 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             }
         }
         if (threadIdx.x == 0) {
-            while (ld_acquire_gpu_u32(&st->turn) == s_turn0) __nanosleep(32);
+            uint64_t t0 = 0;
+            while (ld_acquire_gpu_u32(&st->turn) == s_turn0) {
+                __nanosleep(32);
+                if (expired(t0, p.timeout)) {        // blocks not co-resident
+                    peer_fail(p.ctl, PEER_ERR_GRID, 1);
+                    break;
+                }
+            }
             s_dc = vst->dc;
             // read: block 0 may now reset the solver state (end of P3)
             atomicAdd(&st->block_counter, 1u);
@@ -546,13 +599,20 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
             // store into them over NVLink), then releases a local "every rank
             // published R" word (ctl[3]) and their accept bits (ctl[4]) for the
             // other blocks
-            const uint32_t mask = wait_flags(p.flags_in, p.world, R);
+            const uint32_t mask = wait_flags(p.flags_in, p.world, R, p.ctl, p.timeout);
             s_acc = mask;
             p.ctl[4] = (int64_t)mask;
             __threadfence();
             atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 3), (unsigned long long)R);
         } else {
-            while ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) < R) __nanosleep(32);
+            uint64_t t0 = 0;
+            while ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) < R) {
+                __nanosleep(32);
+                if (expired(t0, 2 * p.timeout)) {    // block 0's own wait has the deadline
+                    peer_fail(p.ctl, PEER_ERR_GRID, 3);
+                    break;
+                }
+            }
             s_acc = (uint32_t)*(volatile int64_t *)(p.ctl + 4);
         }
     }
@@ -579,14 +639,26 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     // f(v), the constant and G(0) of the next round are formed by its P1;
     // block 0 resets the solver state once every block has read the decision
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    while (ld_acquire_gpu_u32(&st->block_counter) < gridDim.x) __nanosleep(32);
+    uint64_t t0 = 0;
+    while (ld_acquire_gpu_u32(&st->block_counter) < gridDim.x) {
+        __nanosleep(32);
+        if (expired(t0, p.timeout)) {
+            peer_fail(p.ctl, PEER_ERR_GRID, 4);
+            break;
+        }
+    }
     st->block_counter = 0;
     tl_end(TL_TURN);
     p.ctl[1] = R;
     if (p.stamps) p.stamps[4] = gtimer();
     if (st->status != GLM_OK) return;          // keep a solver error visible to the host
-    st->gen_state = st->gen_next;              // begin_kernel with reuse_gsum, reset damping
-    st->damping = 1.0;
+    st->gen_state = st->gen_next;              // begin_kernel with reuse_gsum
+    // damping: an accepted (or plateaued) attempt resets it like the
+    // reference's per-round reset (engine.py:251-252); a rejected one keeps
+    // the halved value, so the next round is the retry damped_solve would have
+    // made (solver.py:282-293) and consecutive rejections reach the floor and
+    // GLM_DIVERGENCE (decide_cached) instead of looping at damping 1
+    if (st->epochs_run > 0 || st->plateaued) st->damping = 1.0;
     st->epochs_target = p.epochs;
     st->epochs_run = 0;
     st->retries = 0;
@@ -659,6 +731,20 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
         glm_peer_destroy(p);
         return glm_set_cuda_error(e, "glm_peer_create", __FILE__, __LINE__);
     }
+    // round_turn spins on work of its other blocks, so its grid must be
+    // co-resident: size it from this device's SM count and the kernel's
+    // occupancy (fail rather than risk a deadlock)
+    int sms = 0, occ = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, round_turn_kernel, TURN_THREADS, 0);
+    if (e != cudaSuccess || occ < 1 || sms < 1) {
+        glm_peer_destroy(p);
+        if (e != cudaSuccess) return glm_set_cuda_error(e, "glm_peer_create", __FILE__, __LINE__);
+        return glm_set_error(GLM_USAGE, "round_turn_kernel cannot be resident on this device");
+    }
+    p->turn_blocks = (occ < 2 ? occ : 2) * sms;
+    if (p->turn_blocks > PEER_BLOCKS) p->turn_blocks = PEER_BLOCKS;
     p->ctl = reinterpret_cast<int64_t *>(p->mem);
     p->dv = reinterpret_cast<double *>(p->mem + 256);
     p->flags = p->ctl + 8;
@@ -717,6 +803,24 @@ int glm_peer_stamps(glm_peer *p, uint64_t *device_array) {
     return GLM_OK;
 }
 
+int glm_peer_set_timeout(glm_peer *p, double seconds) {
+    if (!p || !(seconds > 0.0)) return glm_set_error(GLM_USAGE, "bad peer timeout");
+    p->timeout_ns = (uint64_t)(seconds * 1e9);
+    return GLM_OK;
+}
+
+// Synchronises the device, then reads (and with clear != 0 resets) the error
+// word: 0 = no wait timed out; else (kind << 32 | what), kind 1 = rank `what`
+// did not publish in time, kind 2 = the turn's blocks were not co-resident.
+int glm_peer_error(glm_peer *p, int64_t *code_out, int clear) {
+    if (!p || !code_out) return glm_set_error(GLM_USAGE, "null argument");
+    GLM_CUDA_TRY(cudaSetDevice(p->device));
+    GLM_CUDA_TRY(cudaDeviceSynchronize());
+    GLM_CUDA_TRY(cudaMemcpy(code_out, p->ctl + 7, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (clear && *code_out) GLM_CUDA_TRY(cudaMemset(p->ctl + 7, 0, sizeof(int64_t)));
+    return GLM_OK;
+}
+
 int glm_peer_consume(glm_peer *p, void *stream) {
     if (!p) return glm_set_error(GLM_USAGE, "null peer");
     count_launch();
@@ -757,6 +861,7 @@ int glm_round_start(glm_peer *p, glm_solver *s, int mode, int kind, double lam,
     a.view1 = s ? s->view[1] : nullptr;
     a.epochs = epochs;
     a.scratch = scratch;
+    a.timeout = p->timeout_ns;
     const bool timed = s && s->timing;
     if (timed) {
         int rc = glue_begin(s, 1, (cudaStream_t)stream);
@@ -813,14 +918,15 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
     a.epochs = epochs;
     a.scratch = scratch;
     a.stamps = p->stamps;
+    a.timeout = p->timeout_ns;
     cudaStream_t st = (cudaStream_t)stream;
     if (s->timing) {
         int rc = glue_begin(s, 2, st);
         if (rc) return rc;
     }
     count_launch();
-    GLM_CUDA_TRY(launch_pdl(true, round_turn_kernel, dim3(PEER_BLOCKS), dim3(TURN_THREADS), 0, st,
-                            a));
+    GLM_CUDA_TRY(launch_pdl(true, round_turn_kernel, dim3(p->turn_blocks), dim3(TURN_THREADS), 0,
+                            st, a));
     if (s->timing) return glue_end(s, st);
     return GLM_OK;
 }

@@ -174,7 +174,7 @@ class Engine:
     def __init__(self, matrix, spec, config, reducer=None, cost_model=None, node_index=None,
                  measure_theta_bar=False, measure_theta_outer=False, chunk_runner=None,
                  mode=None, sync_solves=True, retry_budget=2, group_lanes=0, max_inflight=0,
-                 n_total=None, cache_flags=0, peer_exchange=True):
+                 n_total=None, cache_flags=0, peer_exchange=True, peer_timeout=None):
         if measure_theta_bar or measure_theta_outer:
             raise ValueError("theta measurement is the reference's CPU test-mode oracle "
                              "(solver.py:308-391); it is out of scope on the device path")
@@ -265,15 +265,22 @@ class Engine:
         self._pending = False
         self._turn_ready = False    # the last glm_round_turn already started the next round
         if (peer_exchange and len(self.workers) == 1 and config.t2 == 1
-                and chunk_runner is None and not self.sync_solves
-                and (self.reducer is None or getattr(self.reducer, "on_cuda", False))):
-            from .comm import PeerExchange
-            try:
-                self.exchange = PeerExchange(self.d, local=self.reducer is None)
-            except Exception:          # no P2P between the ranks' GPUs: NCCL path
+                and chunk_runner is None and not self.sync_solves):
+            from .comm import PeerExchange, ReduceError
+            try:       # collective: every rank gets an exchange or none does
+                self.exchange = PeerExchange(self.d, local=self.reducer is None,
+                                             timeout=peer_timeout)
+            except ReduceError:        # no P2P between the ranks' GPUs: NCCL path
                 self.exchange = None
             if self.exchange is not None:
                 self.exchange.consume(self.stream)
+
+    def close(self):
+        """Release the peer exchange (IPC mappings) before the process group
+        or the CUDA context goes away."""
+        if self.exchange is not None:
+            self.exchange.close()
+            self.exchange = None
 
     # -- state -----------------------------------------------------------------
     def _initial_v(self):
@@ -528,6 +535,13 @@ class Engine:
     def check_solves(self):
         """Raise the solver error of the last round's subtasks (deferred when
         solves are enqueued without a host round-trip, sync_solves=False)."""
+        if self.exchange is not None:
+            try:
+                self.exchange.check()          # a device-side wait that timed out
+            except BaseException:
+                if self.reducer is not None and hasattr(self.reducer, "abort"):
+                    self.reducer.abort()
+                raise
         if self.sync_solves or self.chunk_runner is not None:
             return
         for wk in self.workers.values():

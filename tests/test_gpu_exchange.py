@@ -81,13 +81,51 @@ def test_fused_round_reset_and_graph_replay():
     np.testing.assert_array_equal(eng.v, v_eager)
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def _torchrun(*extra, timeout=600):
+    return subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+         os.path.join(ROOT, "tests", "mp_exchange_check.py"), *extra],
+        capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+
+
 def test_two_process_exchange_matches_nccl():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    out = subprocess.run(
-        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-         "--master-addr", "127.0.0.1", "--master-port", "29533",
-         os.path.join(ROOT, "tests", "mp_exchange_check.py")],
-        capture_output=True, text=True, timeout=300, cwd=ROOT)
+    out = _torchrun()
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
+    assert "GRAPH async OK" in out.stdout, out.stdout[-2000:]
+
+
+def test_two_process_exchange_same_gpu():
+    """Both ranks on cuda:0 (gloo bootstrap, time-sliced contexts): the IPC
+    mappings, the pushed flag words, the parity double buffer and the
+    rank-ordered sum of csrc/peer.cu across two processes, bit-identical to the
+    deterministic reducer and to the in-process K = 2 engine; then the benched
+    kernel configuration (async, cache_flags=1, fused turn) replayed from a
+    CUDA graph across the ranks, with v = A alpha afterwards."""
+    out = _torchrun("--same-gpu")
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
+    assert "GRAPH sequential OK" in out.stdout and "GRAPH async OK" in out.stdout, \
+        out.stdout[-2000:]
+
+
+def test_dead_rank_surfaces_as_error():
+    """Rank 1 dies mid-training; rank 0's device-side waits hit their deadline
+    (3 s here; the reference's DEFAULT_TIMEOUT is 60 s, comm.py:30) and the
+    engine raises instead of spinning forever (engine.py:284-288)."""
+    out = _torchrun("--same-gpu", "--kill", timeout=300)
+    assert "TIMEOUT OK" in out.stdout or "TIMEOUT CUDA" in out.stdout, \
+        out.stdout[-3000:] + out.stderr[-3000:]
+    assert "NO ERROR" not in out.stdout

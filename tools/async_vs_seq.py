@@ -36,4 +36,5 @@ if rank == 0:
     out["within_10pct"] = abs(a - s) <= max(1, 0.1 * s)
     print(json.dumps(out), flush=True)
 sys.stdout.flush()
-os._exit(0)
+from paper_1803_06333_b200.comm import shutdown  # noqa: E402
+shutdown()

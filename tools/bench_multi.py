@@ -244,9 +244,9 @@ def main():
         if args.out:
             with open(args.out, "a") as fh:
                 fh.write(line + "\n")
-    torch.cuda.synchronize()
     sys.stdout.flush()
-    os._exit(0)
+    from paper_1803_06333_b200.comm import shutdown
+    shutdown()
 
 
 if __name__ == "__main__":

@@ -62,4 +62,5 @@ if world > 1:
               round(float(np.median(W.min(0))), 2), "| median of max over ranks:",
               round(float(np.median(W.max(0))), 2))
 sys.stdout.flush()
-os._exit(0)
+from paper_1803_06333_b200.comm import shutdown  # noqa: E402
+shutdown()
