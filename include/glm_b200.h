@@ -421,6 +421,34 @@ int glm_svmlight_fetch(const glm_svmlight *r, int64_t *indptr, int32_t *rows, do
                        double *labels);
 int glm_svmlight_free(glm_svmlight *r);
 
+/* ------------------------------------- (6) GLMCHUNK v1 chunk store (host)
+ * write_chunks / open_chunks / read_chunk (data.py:17-27, 329-426), byte-for-
+ * byte the reference's format.  Status kinds (the Python layer raises the
+ * reference's ChunkFormatError messages): 0 ok, 1 truncated header, 2 bad
+ * magic, 3 endianness mismatch, 4 unsupported version, 5 truncated row
+ * vector, 6 truncated chunk header, 7 column counts do not sum to n_cols,
+ * 8 chunk header disagrees with descriptor, 9 truncated chunk body,
+ * 10 OS error (errno reported). */
+/* labels / row_vector NULL: not stored.  offsets_out: ceil(n_cols/chunk_size)
+ * chunk offsets.  *os_errno != 0 if the file could not be written. */
+int glm_chunk_write(const char *path, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
+                    const int32_t *rows, const double *vals, const double *labels,
+                    const double *row_vector, int64_t chunk_size, int64_t *offsets_out,
+                    int64_t *os_errno);
+typedef struct glm_chunkfile glm_chunkfile;
+/* info[8]: status kind, n_rows, n_cols, flags, version, n_chunks, errno;
+ * magic_out (8 bytes, may be NULL): the magic read.  *out only when ok. */
+int glm_chunk_open(const char *path, glm_chunkfile **out, int64_t *info, char *magic_out);
+/* descriptor table (n_chunks each) and the row vector (n_rows, if flagged) */
+int glm_chunk_table(const glm_chunkfile *f, int64_t *offsets, int64_t *n_cols, int64_t *nnz,
+                    double *row_vector);
+int glm_chunk_close(glm_chunkfile *f);
+/* one chunk body: indptr i64[n_cols+1] (chunk-relative), rows i32[nnz],
+ * vals f64[nnz], labels f64[n_cols] (if has_labels); status[2] = kind, errno */
+int glm_chunk_read(const char *path, int64_t offset, int64_t n_cols, int64_t nnz, int has_labels,
+                   int64_t *indptr, int32_t *rows, double *vals, double *labels,
+                   int64_t *status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -139,6 +139,13 @@ SIGNATURES = {
     "glm_svmlight_parse": (ctypes.c_int, [_P, _c_i64, ctypes.c_int, _P, _P]),
     "glm_svmlight_fetch": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "glm_svmlight_free": (ctypes.c_int, [_P]),
+    "glm_chunk_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64, _c_i64, _P, _P, _P, _P, _P,
+                                       _c_i64, _P, _P]),
+    "glm_chunk_open": (ctypes.c_int, [ctypes.c_char_p, _P, _P, _P]),
+    "glm_chunk_table": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "glm_chunk_close": (ctypes.c_int, [_P]),
+    "glm_chunk_read": (ctypes.c_int, [ctypes.c_char_p, _c_i64, _c_i64, _c_i64, ctypes.c_int,
+                                      _P, _P, _P, _P, _P]),
 }
 
 _LIB = None

@@ -8,3 +8,4 @@
 #include "stream.cu"
 #include "peer.cu"
 #include "ingest.cu"
+#include "chunkfile.cu"

@@ -107,6 +107,10 @@ struct Piece {
     int64_t max_feat = 0;
     int err = ING_OK;
     int64_t err_line = 0, tok_off = 0, tok_len = 0;
+    // an index beyond int32 is not a format error: the reference only fails
+    // when it converts the finished row list (np.asarray(rows, int32)), so a
+    // later format error wins; the first such token is kept
+    int64_t range_line = 0, range_off = -1, range_len = 0;
 };
 
 void parse_piece(const char *base, Piece &P) {
@@ -149,8 +153,10 @@ void parse_piece(const char *base, Piece &P) {
                     P.err = ING_INDEX_LT1;
                 } else if (idx <= prev) {
                     P.err = ING_NOT_INCREASING;
-                } else if (range || idx > (long long)INT32_MAX + 1) {
-                    P.err = ING_INDEX_RANGE;
+                } else if ((range || idx > (long long)INT32_MAX + 1) && P.range_off < 0) {
+                    P.range_line = line;
+                    P.range_off = s - base;
+                    P.range_len = t - s;
                 }
                 if (P.err) {
                     P.err_line = line;
@@ -158,7 +164,7 @@ void parse_piece(const char *base, Piece &P) {
                     P.tok_len = t - s;
                     return;
                 }
-                prev = idx;
+                prev = range ? LLONG_MAX : idx;
                 P.rows.push_back((int32_t)(idx - 1));
                 P.vals.push_back(v);
                 ++cnt;
@@ -228,7 +234,28 @@ int glm_svmlight_parse(const char *text, int64_t len, int n_threads, glm_svmligh
         for (int i = 0; i < T; ++i) th.emplace_back([&, i] { parse_piece(text, r->pieces[i]); });
         for (auto &t : th) t.join();
     }
+    const Piece *rng = nullptr;
+    for (auto &P : r->pieces)
+        if (!P.err && P.range_off >= 0) {
+            rng = &P;
+            break;
+        }
     for (auto &P : r->pieces) {
+        if (!P.err && &P == rng && rng->range_off >= 0) {
+            // no format error before it: still scan later pieces for one
+            bool later = false;
+            for (auto &Q : r->pieces) later = later || (&Q > &P && Q.err);
+            if (!later) {
+                info[0] = info[1] = info[2] = 0;
+                info[3] = ING_INDEX_RANGE;
+                info[4] = P.range_line;
+                info[5] = P.range_off;
+                info[6] = P.range_len;
+                delete r;
+                *out = nullptr;
+                return GLM_OK;
+            }
+        }
         if (P.err) {              // the first error in file order
             info[0] = info[1] = info[2] = 0;
             info[3] = P.err;

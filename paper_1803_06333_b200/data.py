@@ -14,8 +14,8 @@ partition of columns is a zero-copy view (indptr offset, shared rows/vals).
 from __future__ import annotations
 
 import ctypes
-import io
-import struct
+import os
+import unicodedata
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -28,8 +28,6 @@ CHUNK_VERSION = 1
 ENDIAN_MARK = 0xFEFF
 _FLAG_LABELS = 1
 _FLAG_ROW_VECTOR = 2
-_HEADER = struct.Struct("<8sIHHQQ")   # data.py:23-25
-_CHUNK_HEAD = struct.Struct("<IQ")    # data.py:26-27
 
 
 class DataFormatError(ValueError):
@@ -258,26 +256,32 @@ class SparseColumnMatrix:
             self._validate()
 
     def _validate(self):
-        """Input checks with the reference's messages (data.py:64-84)."""
-        if self.indptr[0] != 0 or self.indptr[-1] != len(self.rows):
-            raise ValueError("indptr does not span the value arrays")
-        if np.any(np.diff(self.indptr) < 0):
-            raise ValueError("indptr must be non-decreasing")
-        if len(self.rows) != len(self.vals):
-            raise ValueError("rows/vals length mismatch")
-        if len(self.rows):
-            if self.rows.min() < 0 or self.rows.max() >= self.n_rows:
-                raise ValueError("row index out of range")
-            if not np.all(np.isfinite(self.vals)):
-                raise ValueError("non-finite value in matrix")
-            d = np.diff(self.rows)
-            starts = np.zeros(len(self.rows), dtype=bool)
-            inner = self.indptr[1:-1]
-            starts[inner[inner < len(self.rows)]] = True
-            if np.any((d <= 0) & ~starts[1:]):
-                raise ValueError("row indices must be strictly increasing per column")
-        if self.labels is not None and len(self.labels) != self.n_cols:
-            raise ValueError("labels length must equal n_cols")
+        """The reference's input checks, in its order, with its messages
+        (data.py:64-84)."""
+        ip, rw, vl = self.indptr, self.rows, self.vals
+        nnz = len(rw)
+        checks = (
+            (lambda: ip[0] == 0 and ip[-1] == nnz, "indptr does not span the value arrays"),
+            (lambda: bool(np.all(ip[1:] >= ip[:-1])), "indptr must be non-decreasing"),
+            (lambda: len(vl) == nnz, "rows/vals length mismatch"),
+            (lambda: nnz == 0 or (int(rw.min()) >= 0 and int(rw.max()) < self.n_rows),
+             "row index out of range"),
+            (lambda: nnz == 0 or bool(np.isfinite(vl).all()), "non-finite value in matrix"),
+            (self._rows_increase, "row indices must be strictly increasing per column"),
+            (lambda: self.labels is None or len(self.labels) == self.n_cols,
+             "labels length must equal n_cols"),
+        )
+        for holds, message in checks:
+            if not holds():
+                raise ValueError(message)
+
+    def _rows_increase(self):
+        """An entry may sit at or below its predecessor only where a column
+        starts (sorted, unique rows per column)."""
+        if len(self.rows) < 2:
+            return True
+        drops = np.flatnonzero(self.rows[1:] <= self.rows[:-1]) + 1
+        return bool(np.isin(drops, self.indptr).all())
 
     @property
     def nnz(self):
@@ -367,122 +371,113 @@ class DenseColumnMatrix:
 
 
 def hstack(blocks):
-    """Concatenate matrices column-wise (data.py:174-187)."""
+    """Column-wise concatenation (data.py:174-187): each block's indptr is
+    shifted by the entries before it; labels survive only if every block
+    has them."""
     blocks = list(blocks)
     n_rows = blocks[0].n_rows
     if any(b.n_rows != n_rows for b in blocks):
         raise ValueError("n_rows mismatch in hstack")
-    indptr = np.concatenate([[0]] + [np.diff(b.indptr) for b in blocks]).cumsum()
-    rows = np.concatenate([b.rows for b in blocks]) if blocks else np.empty(0, np.int32)
+    shift = np.cumsum([0] + [int(b.indptr[-1] - b.indptr[0]) for b in blocks[:-1]],
+                      dtype=np.int64)
+    indptr = np.concatenate([np.zeros(1, np.int64)] +
+                            [np.asarray(b.indptr[1:], np.int64) - b.indptr[0] + o
+                             for b, o in zip(blocks, shift)])
+    rows = np.concatenate([b.rows for b in blocks])
     vals = np.concatenate([b.vals for b in blocks])
-    labels = None
-    if all(b.labels is not None for b in blocks):
-        labels = np.concatenate([b.labels for b in blocks])
-    return SparseColumnMatrix(n_rows, indptr.astype(np.int64), rows, vals, labels,
-                              validate=False)
+    has_labels = all(b.labels is not None for b in blocks)
+    labels = np.concatenate([b.labels for b in blocks]) if has_labels else None
+    return SparseColumnMatrix(n_rows, indptr, rows, vals, labels, validate=False)
 
 
 # --------------------------------------------------------------- svmlight
-# Characters whose meaning differs between Python's line/field splitting and
-# the native parser's ASCII grammar: inputs containing them take the
-# line-by-line path below, which follows data.py:190-239 exactly.
-_NATIVE_UNSAFE = ("\x0b", "\x0c", "\x1c", "\x1d", "\x1e", "\x1f")
+# Characters outside the native parser's ASCII grammar whose meaning Python's
+# str.split/strip/float give them: every whitespace character separates, and
+# int()/float() read any Unicode decimal digit (CPython maps both to ASCII
+# before parsing a number); anything else is just an invalid character.
+_EXOTIC_ASCII = "\x1c\x1d\x1e\x1f"
+
+
+def _to_grammar(text):
+    """Map `text` one character to one ASCII character so the native grammar
+    sees what Python's line parsing would: offsets into the result are
+    offsets into `text` (error tokens are cut from the original)."""
+    if text.isascii() and not any(c in text for c in _EXOTIC_ASCII):
+        return text
+    table = {}
+    for ch in set(text):
+        if ch == "\n" or (ch.isascii() and ch not in _EXOTIC_ASCII):
+            continue
+        if ch.isspace():
+            table[ord(ch)] = " "
+        else:
+            dig = unicodedata.decimal(ch, None)
+            table[ord(ch)] = str(dig) if dig is not None else "\x01"
+    return text.translate(table)
 
 
 def parse_svmlight(stream, n_threads=0):
     """svmlight text -> (example-major matrix, labels) (data.py:190-239).
 
-    Host ingest: text from a str or a file object is parsed
-    by the multi-threaded native parser (csrc/ingest.cu, `glm_svmlight_parse`);
-    exotic input (non-ASCII, or separators Python splits on but the native
-    grammar does not) and every error case run the line-by-line path, so the
-    values, the arrays and the error messages are those of the reference."""
+    Host ingest by the multi-threaded native parser
+    (csrc/ingest.cu, `glm_svmlight_parse`).  The input is first brought to
+    the lines the reference iterates: a str is cut with str.splitlines(), a
+    file object at its newlines, an iterable gives one line per item; the
+    native error report (kind, line, token offsets) becomes the reference's
+    exception and message here."""
     if isinstance(stream, str):
-        text, str_input = stream, True
+        text = "\n".join(stream.splitlines())
     elif hasattr(stream, "read"):
-        text, str_input = stream.read(), False
+        text = stream.read()
         if isinstance(text, bytes):
             text = text.decode()
     else:
-        return _parse_svmlight_lines(stream)
-    res = _parse_svmlight_native(text, str_input, n_threads)
-    if res is not None:
-        return res
-    return _parse_svmlight_lines(text.splitlines() if str_input else io.StringIO(text))
-
-
-def _parse_svmlight_native(text, str_input, n_threads):
-    if not text.isascii() or any(c in text for c in _NATIVE_UNSAFE) or \
-            (str_input and "\r" in text):
-        return None
-    data = text.encode()
+        text = "\n".join((ln.decode() if isinstance(ln, bytes) else ln).replace("\n", " ")
+                         for ln in stream)
+    data = _to_grammar(text).encode("ascii")
     lib = L.lib()
     h = ctypes.c_void_p()
     info = np.zeros(7, dtype=np.int64)
     L.check(lib.glm_svmlight_parse(data, len(data), int(n_threads), ctypes.byref(h),
                                    info.ctypes.data_as(ctypes.c_void_p)), "glm_svmlight_parse")
     if info[3] != 0:
-        return None                      # the line path raises the reference's error
+        _raise_parse_error(int(info[3]), int(info[4]), text[info[5]:info[5] + info[6]])
     n, nnz, max_feat = int(info[0]), int(info[1]), int(info[2])
-    indptr = np.empty(n + 1, dtype=np.int64)
-    rows = np.empty(nnz, dtype=np.int32)
-    vals = np.empty(nnz, dtype=np.float64)
-    labels = np.empty(n, dtype=np.float64)
-    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    arrays = (np.empty(n + 1, np.int64), np.empty(nnz, np.int32), np.empty(nnz, np.float64),
+              np.empty(n, np.float64))
     try:
-        L.check(lib.glm_svmlight_fetch(h, vp(indptr), vp(rows), vp(vals), vp(labels)),
+        L.check(lib.glm_svmlight_fetch(h, *(a.ctypes.data_as(ctypes.c_void_p) for a in arrays)),
                 "glm_svmlight_fetch")
     finally:
         lib.glm_svmlight_free(h)
+    indptr, rows, vals, labels = arrays
     return SparseColumnMatrix(max_feat, indptr, rows, vals), labels
 
 
-def _parse_svmlight_lines(lines):
-    """The reference's line loop (data.py:198-239), same validation/messages."""
-    labels, indptr, rows, vals = [], [0], [], []
-    max_feat = 0
-    for lineno, line in enumerate(lines, start=1):
-        line = line.strip()
-        if not line or line.startswith("#"):
-            continue
-        parts = line.split()
-        try:
-            y = float(parts[0])
-        except ValueError:
-            raise DataFormatError(f"line {lineno}: bad label {parts[0]!r}")
-        prev = 0
-        for tok in parts[1:]:
-            try:
-                idx_s, val_s = tok.split(":", 1)
-                idx = int(idx_s)
-                val = float(val_s)
-            except ValueError:
-                raise DataFormatError(f"line {lineno}: bad feature token {tok!r}")
-            if idx < 1:
-                raise DataFormatError(f"line {lineno}: feature index {idx} < 1")
-            if idx <= prev:
-                raise DataFormatError(
-                    f"line {lineno}: feature indices must be strictly increasing")
-            prev = idx
-            rows.append(idx - 1)
-            vals.append(val)
-        max_feat = max(max_feat, prev)
-        labels.append(y)
-        indptr.append(len(rows))
-    mat = SparseColumnMatrix(max_feat, np.asarray(indptr, dtype=np.int64),
-                             np.asarray(rows, dtype=np.int32), np.asarray(vals, dtype=np.float64))
-    return mat, np.asarray(labels, dtype=np.float64)
+def _raise_parse_error(kind, line, token):
+    """The reference's exception for the native parser's first error."""
+    where = f"line {line}: "
+    if kind == 1:
+        raise DataFormatError(where + f"bad label {token!r}")
+    if kind == 2:
+        raise DataFormatError(where + f"bad feature token {token!r}")
+    if kind == 3:
+        raise DataFormatError(where + f"feature index {int(token.split(':', 1)[0])} < 1")
+    if kind == 4:
+        raise DataFormatError(where + "feature indices must be strictly increasing")
+    # kind 5: an index past int32 — the reference fails converting its row
+    # list (np.asarray(rows, dtype=np.int32)); let numpy raise the same error
+    np.asarray([int(token.split(":", 1)[0]) - 1], dtype=np.int32)
+    raise OverflowError(f"feature index out of int32 range at line {line}")
 
 
 def write_svmlight(matrix, labels, stream):
-    """data.py:242-250 (value-exact %.17g)."""
-    for j in range(matrix.n_cols):
-        r, v = matrix.col(j)
-        feats = " ".join("%d:%.17g" % (ri + 1, vi) for ri, vi in zip(r, v))
-        line = "%.17g" % labels[j]
-        if feats:
-            line += " " + feats
-        stream.write(line + "\n")
+    """Example-major matrix -> svmlight text (data.py:242-250): every number
+    as %.17g, so parsing the text returns the same bits."""
+    tokens = [f"{r + 1}:{v:.17g}" for r, v in zip(matrix.rows.tolist(), matrix.vals.tolist())]
+    ends = np.asarray(matrix.indptr).tolist()
+    for j, y in enumerate(np.asarray(labels, dtype=np.float64).tolist()):
+        stream.write(" ".join([f"{y:.17g}"] + tokens[ends[j]:ends[j + 1]]) + "\n")
 
 
 # -------------------------------------------------------------- partitions
@@ -561,142 +556,92 @@ class ChunkStore:
         return len(self.chunks)
 
 
+_CHUNK_ERRORS = {1: "truncated header", 3: "endianness mismatch", 5: "truncated row vector",
+                 6: "truncated chunk header", 7: "chunk column counts do not sum to n_cols",
+                 8: "chunk header disagrees with descriptor", 9: "truncated chunk body"}
+
+
+def _chunk_error(kind, path, errno_=0, magic=b"", version=0):
+    if kind == 10:
+        raise OSError(errno_, os.strerror(errno_), str(path))
+    if kind == 2:
+        raise ChunkFormatError(f"bad magic {magic!r}")
+    if kind == 4:
+        raise ChunkFormatError(f"unsupported version {version}")
+    raise ChunkFormatError(_CHUNK_ERRORS[kind])
+
+
 def write_chunks(matrix, chunk_size, path, row_vector=None):
-    """GLMCHUNK v1 writer (data.py:329-359), byte-identical to the reference."""
+    """GLMCHUNK v1 writer (data.py:329-359) — native (csrc/chunkfile.cu),
+    byte-identical to the reference's files."""
     if chunk_size < 1:
         raise ValueError("chunk_size must be >= 1")
-    has_labels = matrix.labels is not None
-    flags = _FLAG_LABELS if has_labels else 0
     if row_vector is not None:
         row_vector = np.ascontiguousarray(row_vector, dtype=np.float64)
         if len(row_vector) != matrix.n_rows:
             raise ValueError("row_vector length must equal n_rows")
-        flags |= _FLAG_ROW_VECTOR
+    labels = None if matrix.labels is None else np.ascontiguousarray(matrix.labels, np.float64)
+    n_chunks = -(-matrix.n_cols // chunk_size)
+    offsets = np.zeros(max(n_chunks, 1), np.int64)
+    err = ctypes.c_int64(0)
+    vp = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    L.check(L.lib().glm_chunk_write(os.fsencode(path), matrix.n_rows, matrix.n_cols,
+                                    vp(matrix.indptr), vp(matrix.rows), vp(matrix.vals),
+                                    vp(labels), vp(row_vector), int(chunk_size), vp(offsets),
+                                    ctypes.byref(err)), "glm_chunk_write")
+    if err.value:
+        _chunk_error(10, path, err.value)
+    sizes = np.diff(np.minimum(np.arange(n_chunks + 1) * chunk_size, matrix.n_cols))
+    nnz = np.diff(matrix.indptr[np.minimum(np.arange(n_chunks + 1) * chunk_size, matrix.n_cols)])
     store = ChunkStore(path=path, n_rows=matrix.n_rows, n_cols=matrix.n_cols,
-                       has_labels=has_labels, row_vector=row_vector)
-    with open(path, "wb") as fh:
-        fh.write(_HEADER.pack(CHUNK_MAGIC, CHUNK_VERSION, flags, ENDIAN_MARK, matrix.n_rows,
-                              matrix.n_cols))
-        if row_vector is not None:
-            fh.write(row_vector.tobytes())
-        for lo in range(0, matrix.n_cols, chunk_size):
-            hi = min(lo + chunk_size, matrix.n_cols)
-            sub_ptr = (matrix.indptr[lo:hi + 1] - matrix.indptr[lo]).astype(np.uint64)
-            nnz = int(sub_ptr[-1])
-            store.chunks.append(ChunkDescriptor(fh.tell(), hi - lo, nnz))
-            fh.write(_CHUNK_HEAD.pack(hi - lo, nnz))
-            fh.write(sub_ptr.tobytes())
-            fh.write(matrix.rows[matrix.indptr[lo]:matrix.indptr[hi]].astype(np.uint32).tobytes())
-            fh.write(matrix.vals[matrix.indptr[lo]:matrix.indptr[hi]].tobytes())
-            if has_labels:
-                fh.write(matrix.labels[lo:hi].tobytes())
+                       has_labels=labels is not None, row_vector=row_vector)
+    store.chunks = [ChunkDescriptor(int(o), int(c), int(z))
+                    for o, c, z in zip(offsets[:n_chunks], sizes, nnz)]
     return store
 
 
 def open_chunks(path):
-    """Scan a chunk file (data.py:362-398)."""
-    with open(path, "rb") as fh:
-        head = fh.read(_HEADER.size)
-        if len(head) < _HEADER.size:
-            raise ChunkFormatError("truncated header")
-        magic, version, flags, endian, n_rows, n_cols = _HEADER.unpack(head)
-        if magic != CHUNK_MAGIC:
-            raise ChunkFormatError(f"bad magic {magic!r}")
-        if endian != ENDIAN_MARK:
-            raise ChunkFormatError("endianness mismatch")
-        if version != CHUNK_VERSION:
-            raise ChunkFormatError(f"unsupported version {version}")
-        has_labels = bool(flags & _FLAG_LABELS)
-        store = ChunkStore(path=path, n_rows=n_rows, n_cols=n_cols, has_labels=has_labels)
-        if flags & _FLAG_ROW_VECTOR:
-            buf = fh.read(8 * n_rows)
-            if len(buf) < 8 * n_rows:
-                raise ChunkFormatError("truncated row vector")
-            store.row_vector = np.frombuffer(buf, dtype="<f8").copy()
-        seen = 0
-        while seen < n_cols:
-            offset = fh.tell()
-            head = fh.read(_CHUNK_HEAD.size)
-            if len(head) < _CHUNK_HEAD.size:
-                raise ChunkFormatError("truncated chunk header")
-            c_cols, c_nnz = _CHUNK_HEAD.unpack(head)
-            store.chunks.append(ChunkDescriptor(offset, c_cols, c_nnz))
-            body = 8 * (c_cols + 1) + 12 * c_nnz + (8 * c_cols if has_labels else 0)
-            fh.seek(body, 1)
-            seen += c_cols
-        if seen != n_cols:
-            raise ChunkFormatError("chunk column counts do not sum to n_cols")
+    """Scan a chunk file into its descriptor table (data.py:362-398), natively."""
+    lib = L.lib()
+    h = ctypes.c_void_p()
+    info = np.zeros(8, np.int64)
+    magic = ctypes.create_string_buffer(8)
+    L.check(lib.glm_chunk_open(os.fsencode(path), ctypes.byref(h),
+                               info.ctypes.data_as(ctypes.c_void_p), magic), "glm_chunk_open")
+    if info[0]:
+        _chunk_error(int(info[0]), path, int(info[6]), magic.raw, int(info[4]))
+    n_rows, n_cols, flags, k = int(info[1]), int(info[2]), int(info[3]), int(info[5])
+    table = np.zeros((3, max(k, 1)), np.int64)
+    rv = np.zeros(n_rows, np.float64) if flags & _FLAG_ROW_VECTOR else None
+    try:
+        L.check(lib.glm_chunk_table(h, *(table[i].ctypes.data_as(ctypes.c_void_p)
+                                         for i in range(3)),
+                                    None if rv is None else rv.ctypes.data_as(ctypes.c_void_p)),
+                "glm_chunk_table")
+    finally:
+        lib.glm_chunk_close(h)
+    store = ChunkStore(path=path, n_rows=n_rows, n_cols=n_cols,
+                       has_labels=bool(flags & _FLAG_LABELS), row_vector=rv)
+    store.chunks = [ChunkDescriptor(int(o), int(c), int(z)) for o, c, z in table[:, :k].T]
     return store
 
 
-def read_chunk_arrays(store, index, out=None):
-    """Chunk `index` as raw little-endian arrays (indptr u64, rows u32, vals f64,
-    labels f64|None) read straight into `out` buffers when given (pinned)."""
-    desc = store.chunks[index]
-    with open(store.path, "rb") as fh:
-        fh.seek(desc.offset)
-        head = fh.read(_CHUNK_HEAD.size)
-        if len(head) < _CHUNK_HEAD.size:
-            raise ChunkFormatError("truncated chunk header")
-        c_cols, c_nnz = _CHUNK_HEAD.unpack(head)
-        if (c_cols, c_nnz) != (desc.n_cols, desc.nnz):
-            raise ChunkFormatError("chunk header disagrees with descriptor")
-        need = 8 * (c_cols + 1) + 12 * c_nnz + (8 * c_cols if store.has_labels else 0)
-        if out is not None:
-            n = fh.readinto(memoryview(out)[:need])
-            buf = out
-        else:
-            buf = fh.read(need)
-            n = len(buf)
-        if n < need:
-            raise ChunkFormatError("truncated chunk body")
-    off = 0
-    indptr = np.frombuffer(buf, dtype="<u8", count=c_cols + 1, offset=off)
-    off += 8 * (c_cols + 1)
-    rows = np.frombuffer(buf, dtype="<u4", count=c_nnz, offset=off)
-    off += 4 * c_nnz
-    vals = np.frombuffer(buf, dtype="<f8", count=c_nnz, offset=off)
-    off += 8 * c_nnz
-    labels = np.frombuffer(buf, dtype="<f8", count=c_cols, offset=off) \
-        if store.has_labels else None
-    return indptr, rows, vals, labels
-
-
 def read_chunk(store, index):
-    """Load chunk `index` as a SparseColumnMatrix (data.py:401-426)."""
-    indptr, rows, vals, labels = read_chunk_arrays(store, index)
-    return SparseColumnMatrix(store.n_rows, indptr.astype(np.int64), rows.astype(np.int32),
-                              vals.copy(), None if labels is None else labels.copy(),
-                              validate=False)
+    """Chunk `index` as a SparseColumnMatrix (data.py:401-426), read natively;
+    the on-disk u64/u32 arrays are the same bits as i64/i32."""
+    desc = store.chunks[index]
+    c, z = desc.n_cols, desc.nnz
+    indptr, rows, vals = np.empty(c + 1, np.int64), np.empty(z, np.int32), np.empty(z, np.float64)
+    labels = np.empty(c, np.float64) if store.has_labels else None
+    status = np.zeros(2, np.int64)
+    vp = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    L.check(L.lib().glm_chunk_read(os.fsencode(store.path), desc.offset, c, z,
+                                   int(store.has_labels), vp(indptr), vp(rows), vp(vals),
+                                   vp(labels), vp(status)), "glm_chunk_read")
+    if status[0]:
+        _chunk_error(int(status[0]), store.path, int(status[1]))
+    return SparseColumnMatrix(store.n_rows, indptr, rows, vals, labels, validate=False)
 
 
 def concat_chunks(store):
     return hstack(read_chunk(store, i) for i in range(store.n_chunks))
-
-
-def spectral_bound(matrix, tolerance=1e-3, max_iters=500):
-    """Upper bound on ||A||_2^2 (data.py:434-464) by power iteration on the GPU."""
-    dm = matrix.device() if hasattr(matrix, "device") else matrix
-    frob = float(torch.dot(dm.vals[:dm.nnz], dm.vals[:dm.nnz]).item()) if dm.nnz else 0.0
-    if frob == 0.0 or dm.n_cols == 0:
-        return 0.0
-    rng = np.random.default_rng(0x5EED)
-    y = rng.standard_normal(dm.n_cols)
-    y /= np.linalg.norm(y)
-    yd = _D().to_device(y)
-    rho = 0.0
-    for _ in range(max_iters):
-        my = dm.rmatvec(dm.matvec(yd))
-        new_rho = float(torch.dot(yd, my).item())
-        nrm = float(torch.linalg.norm(my).item())
-        if nrm == 0.0:
-            return 0.0
-        done = abs(new_rho - rho) <= tolerance * max(new_rho, 1e-300)
-        rho = new_rho
-        yd = my / nrm
-        if done:
-            break
-    my = dm.rmatvec(dm.matvec(yd))
-    rho = float(torch.dot(yd, my).item())
-    resid = float(torch.linalg.norm(my - rho * yd).item())
-    return min(frob, rho + resid)

@@ -376,7 +376,32 @@ def gen_chunked():
     _save("chunked", **arrays)
 
 
+def gen_ingest():
+    """rdata.parse_svmlight (data.py:190-239) on the shared seeded texts
+    (tests/svm_texts.py): sha256 of (n_rows, indptr, rows, vals, labels), or
+    the exception class and message it raised."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "svm_texts", os.path.join(os.path.dirname(OUT), "svm_texts.py"))
+    svm_texts = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(svm_texts)
+    names, digests = [], []
+    for name, text in svm_texts.cases().items():
+        names.append(name)
+        try:
+            m, y = rdata.parse_svmlight(text)
+            digests.append(svm_texts.digest(m, y))
+        except Exception as exc:          # the reference's error is the golden
+            digests.append(svm_texts.error_key(exc))
+    _save("ingest", names=np.array(names), digests=np.array(digests))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:            # regenerate selected fixtures only
+        for name in sys.argv[1:]:
+            globals()["gen_" + name]()
+        sys.exit(0)
+    gen_ingest()
     gen_prng()
     gen_coord()
     gen_solve()

@@ -66,16 +66,18 @@ def test_wide_dense_ridge_c1_shape():
 
 
 def _epochs_to(gaps, objs, tol):
-    rel = np.asarray(gaps) / np.abs(np.asarray(objs))
-    hit = np.flatnonzero(rel <= tol)
+    """First round whose certified gap is <= tol * |F| (no division: F is 0
+    at alpha = 0 for the SVM dual)."""
+    hit = np.flatnonzero(np.asarray(gaps) <= tol * np.abs(np.asarray(objs)))
     return int(hit[0]) if len(hit) else None
 
 
 @pytest.mark.parametrize("lam", [50.0, 500.0])
 def test_narrow_dense_async_reaches_target_like_sequential(lam):
     """North-star async bar: the async run reaches the deterministic run's
-    duality-gap target within the same number of epochs +-10% (+1 for the
-    integer granularity of a few-epoch count)."""
+    duality-gap target within the same number of epochs +-10% (two-sided; at
+    least one epoch of slack for the integer granularity of a few-epoch
+    count)."""
     A = _higgs(200_000, 28, 9)
     m = g.DenseColumnMatrix(A)
     spec = g.ObjectiveSpec("dual_l2_svm", lam, m.n_cols, m.n_rows)
@@ -85,7 +87,8 @@ def test_narrow_dense_async_reaches_target_like_sequential(lam):
         res = eng.train(g.StoppingCriteria(max_rounds=12))
         runs[mode] = _epochs_to(res.trace.gaps(), res.trace.objectives(), 1e-3)
     assert runs["sequential"] is not None and runs["async"] is not None, runs
-    assert runs["async"] <= int(np.ceil(1.1 * runs["sequential"])) + 1, runs
+    assert abs(runs["async"] - runs["sequential"]) <= max(1, round(0.1 * runs["sequential"])), \
+        runs
 
 
 def test_narrow_dense_async_delta_v_consistent():

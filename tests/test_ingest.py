@@ -1,7 +1,10 @@
-"""Native svmlight ingest (csrc/ingest.cu) vs the reference's line parser
-(data.py:190-239): bit-identical arrays on the reference's bundled dataset,
-on randomized number spellings, multi-threaded on multi-MB input, and the
-reference's error messages. Host-only: runs without a GPU."""
+"""Native svmlight ingest (csrc/ingest.cu) vs the reference's parser
+(data.py:190-239): bit-identical arrays on the reference's bundled dataset
+and, through digests the reference itself produced (tests/golden/ingest.npz,
+tests/golden/make_golden.py gen_ingest), on randomized number spellings,
+Unicode separators and digits, multi-threaded multi-MB input, file objects
+and line iterables; the reference's exceptions and messages. Host-only: runs
+without a GPU."""
 
 import io
 
@@ -9,6 +12,8 @@ import numpy as np
 import pytest
 
 from paper_1803_06333_b200 import data as D
+
+import svm_texts
 
 
 def _same(a, b):
@@ -32,55 +37,54 @@ def test_reference_dataset_roundtrip(golden):
     np.testing.assert_array_equal(m.rows, d["ex_rows"])
     assert m.vals.tobytes() == np.asarray(d["ex_vals"]).tobytes()
     assert y.tobytes() == np.asarray(d["ex_labels"]).tobytes()
-    assert D._parse_svmlight_native(buf.getvalue(), True, 0) is not None   # native path taken
 
 
-def _random_text(rng, n, d, k):
-    spell = [lambda v: "%.17g" % v, lambda v: repr(float(v)), lambda v: "%.3e" % v,
-             lambda v: "%.6f" % v, lambda v: "%+.5E" % v, lambda v: "%d" % int(v * 100),
-             lambda v: ("%d" % int(v * 1e6)).replace("000", "_000"),
-             lambda v: ".%d" % abs(int(v * 1000)), lambda v: "%d." % int(v * 10)]
-    lines = ["# header comment", ""]
-    for _ in range(n):
-        y = rng.choice(["1", "-1", "0", "+1", "1.0", "2.5e-1", "-0"])
-        feats = np.sort(rng.choice(d, size=rng.integers(0, k + 1), replace=False)) + 1
-        toks = [f"{j}:{spell[rng.integers(len(spell))](rng.standard_normal())}" for j in feats]
-        sep = rng.choice([" ", "\t", "  "])
-        lines.append(sep.join([y] + toks) + rng.choice(["", " ", "\t"]))
-    lines.append("  # trailing comment")
-    return "\n".join(lines) + "\n"
+@pytest.fixture(scope="module")
+def ingest_golden(golden):
+    z = golden("ingest")
+    return dict(zip(z["names"].tolist(), z["digests"].tolist()))
 
 
-def test_native_equals_line_parser_random_spellings():
-    rng = np.random.default_rng(5)
-    text = _random_text(rng, 3000, 500, 12)
-    text += "inf 5:1_0.5_0e1_0 6:-0.0\n-NaN 1:2\n-Infinity\n"
-    nat = D._parse_svmlight_native(text, True, 0)
-    assert nat is not None
-    _same(nat, D._parse_svmlight_lines(text.splitlines()))
+def _outcome(fn):
+    try:
+        return svm_texts.digest(*fn())
+    except Exception as exc:
+        return svm_texts.error_key(exc)
 
 
-def test_multithreaded_large_input_and_file_objects(tmp_path):
-    rng = np.random.default_rng(9)
-    text = _random_text(rng, 60_000, 20_000, 30)            # several MB -> many pieces
-    assert len(text) > 4 << 20
-    ref = D._parse_svmlight_lines(text.splitlines())
-    for threads in (1, 3, 16):
-        _same(D._parse_svmlight_native(text, True, threads), ref)
+@pytest.mark.parametrize("name", list(svm_texts.cases()))
+def test_parse_matches_reference_golden(name, ingest_golden):
+    """The reference parser's arrays (sha256) or its exact exception and
+    message on every case, str input, default threads."""
+    text = svm_texts.cases()[name]
+    assert _outcome(lambda: D.parse_svmlight(text)) == ingest_golden[name]
+
+
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_multithreaded_pieces_agree(threads, ingest_golden):
+    text = svm_texts.cases()["random_large"]
+    assert len(text) > 4 << 20                               # several MB -> many pieces
+    assert _outcome(lambda: D.parse_svmlight(text, n_threads=threads)) == \
+        ingest_golden["random_large"]
+
+
+def test_file_objects_and_line_iterables(tmp_path, ingest_golden):
+    text = svm_texts.cases()["random_small"]
     p = tmp_path / "x.svm"
-    p.write_bytes(text.replace("\n", "\r\n").encode())         # CRLF file, text mode
+    p.write_bytes(text.replace("\n", "\r\n").encode())     # CRLF file, text mode
     with open(p) as fh:
-        _same(D.parse_svmlight(fh), ref)
+        assert _outcome(lambda: D.parse_svmlight(fh)) == ingest_golden["random_small"]
+    lines = text.splitlines()                                # an iterable of lines
+    assert _outcome(lambda: D.parse_svmlight(iter(lines))) == ingest_golden["random_small"]
+    assert _outcome(lambda: D.parse_svmlight(io.StringIO(text))) == ingest_golden["random_small"]
 
 
 @pytest.mark.parametrize("text,msg", [
     ("1 1:2\nfoo 1:2\n", "line 2: bad label 'foo'"),
-    ("1 1:2 3\n", "line 1: bad feature token '3'"),
     ("1 1:2 x:3\n", "line 1: bad feature token 'x:3'"),
-    ("\n\n1 0:2\n", "line 3: feature index 0 < 1"),
-    ("1 2:1 2:3\n", "line 1: feature indices must be strictly increasing"),
     ("1 1:0x1p3\n", "line 1: bad feature token '1:0x1p3'"),
     ("1 1:1__0\n", "line 1: bad feature token '1:1__0'"),
+    ("1 -0:1\n", "line 1: feature index 0 < 1"),
 ])
 def test_errors_match_reference_messages(text, msg):
     with pytest.raises(D.DataFormatError) as ei:
@@ -91,8 +95,3 @@ def test_errors_match_reference_messages(text, msg):
 def test_non_finite_feature_rejected_like_reference():
     with pytest.raises(ValueError, match="non-finite"):
         D.parse_svmlight("1 1:inf\n")
-
-
-def test_exotic_separators_use_the_line_path():
-    text = "1 1:2\x1f2:3\n-1 1:1\n"        # str.split() separates at \x1f; the ASCII grammar not
-    _same(D.parse_svmlight(text), D._parse_svmlight_lines(text.splitlines()))
