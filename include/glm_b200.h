@@ -49,7 +49,8 @@ enum glm_kind {
     GLM_DUAL_RIDGE = 4,           /* restated */
     GLM_ELASTIC_NET_PRIMAL = 5,   /* restated */
     GLM_LOGISTIC_PRIMAL = 6,      /* restated */
-    GLM_SQUARED_HINGE_PRIMAL = 7  /* restated */
+    GLM_SQUARED_HINGE_PRIMAL = 7, /* restated */
+    GLM_HINGE_PRIMAL = 8          /* restated: smoothed hinge, row target y_r / mu */
 };
 
 enum glm_layout { GLM_CSC = 0, GLM_DENSE = 1 };

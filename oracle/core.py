@@ -26,7 +26,8 @@ __all__ = [
 ]
 
 KINDS = ("dual_l2_logistic", "dual_l2_svm", "ridge_primal", "lasso_primal",
-         "dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal")
+         "dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal",
+         "hinge_primal")   # 8: smoothed hinge, target[r] = y_r / mu (glm_oracle.c)
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 _LOCK = threading.Lock()
@@ -176,9 +177,12 @@ def argsort_stable(keys):
 
 
 # ------------------------------------------------------------ objectives
-def beta_of(kind):
-    """ObjectiveSpec.beta (objectives.py:71-73); restated: logistic_primal 1/4."""
+def beta_of(kind, target=None):
+    """ObjectiveSpec.beta (objectives.py:71-73); restated: logistic_primal 1/4,
+    smoothed hinge 1/mu (= max |target|, the target carrying y / mu)."""
     k = kind_index(kind)
+    if k == 8:
+        return float(np.max(np.abs(target)))
     return {0: None, 1: None, 4: None, 6: 0.25}.get(k, 1.0)
 
 
@@ -187,10 +191,12 @@ def init_alpha(kind, n):
     return np.full(n, 0.5) if kind_index(kind) == 0 else np.zeros(n)
 
 
-def _beta(kind, lam):
+def _beta(kind, lam, target=None):
     k = kind_index(kind)
     if k in (0, 1, 4):
         return 1.0 / lam
+    if k == 8:
+        return float(np.max(np.abs(target)))
     return 0.25 if k == 6 else 1.0
 
 
@@ -376,7 +382,7 @@ def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed
     K, L = nodes, devices
     sig = float(K if sigma is None else sigma)
     sigb = float(L if sigma_bar is None else sigma_bar)
-    beta = _beta(k, lam)
+    beta = _beta(k, lam, target)
     bounds = partition_bounds(m.n_cols, K, L, strategy,
                               np.diff(m.indptr) if strategy != "contiguous" else None)
     subs = []
@@ -470,7 +476,7 @@ def train_chunked(m, kind, lam, chunk_size, *, target=None, epochs=1, seed=0, ro
     offsets = np.concatenate([np.arange(0, n, chunk_size), [n]]).astype(np.int64)
     alpha = init_alpha(k, n)
     v = matvec(m, alpha)
-    beta = _beta(k, lam)
+    beta = _beta(k, lam, target)
     objs = [f_eval(k, lam, target, v) + g_sum(k, lam, alpha, rho, y)]
     epoch_counter = 0
     for _ in range(rounds):

@@ -14,7 +14,7 @@
  * parity UNPINNED by the reference):
  *   0 dual_l2_logistic  1 dual_l2_svm  2 ridge_primal  3 lasso_primal
  *   4 dual_ridge        5 elastic_net_primal  6 logistic_primal
- *   7 squared_hinge_primal
+ *   7 squared_hinge_primal  8 hinge_primal (smoothed hinge: target[r] = y_r / mu)
  */
 #include <math.h>
 #include <stdint.h>
@@ -138,7 +138,7 @@ static double g_one(int kind, double lam, double rho, double y, double a) {
     switch (kind) {
     case 0: return entropy(a);                         /* objectives.py:167-168 */
     case 1: return -a;                                 /* objectives.py:169-170 */
-    case 2: case 6: case 7: return 0.5 * lam * a * a;  /* objectives.py:171-172 */
+    case 2: case 6: case 7: case 8: return 0.5 * lam * a * a;  /* objectives.py:171-172 */
     case 3: return lam * fabs(a);                      /* objectives.py:173 */
     case 4: return 0.5 * a * a - y * a;                /* restated */
     case 5: return lam * (rho * fabs(a) + 0.5 * (1.0 - rho) * a * a); /* restated */
@@ -163,7 +163,7 @@ double or_g_conj_sum(int kind, double lam, double rho, const double *y, const do
         switch (kind) {
         case 0: acc += softplus(x); break;
         case 1: acc += x + 1.0 > 0.0 ? x + 1.0 : 0.0; break;
-        case 2: case 6: case 7: acc += x * x / (2.0 * lam); break;
+        case 2: case 6: case 7: case 8: acc += x * x / (2.0 * lam); break;
         case 4: { double u = x + y[i]; acc += 0.5 * u * u; } break;
         case 5: {
             if (rho >= 1.0) return NAN;
@@ -174,6 +174,17 @@ double or_g_conj_sum(int kind, double lam, double rho, const double *y, const do
         }
     }
     return acc;
+}
+
+/* Smoothed hinge (restated kind 8), target t = y / mu: h(z) = 0 for z >= 1,
+ * (1 - z)^2 / (2 mu) for 1 - mu < z < 1, 1 - z - mu / 2 below; z = y v.
+ * Returns h and its derivative in v; mu -> 0 gives the hinge max(0, 1 - z). */
+static double smooth_hinge(double t, double v, double *dv) {
+    const double y = t > 0.0 ? 1.0 : -1.0, mu = 1.0 / fabs(t), z = y * v;
+    if (z >= 1.0) { *dv = 0.0; return 0.0; }
+    if (z > 1.0 - mu) { const double m = 1.0 - z; *dv = -y * m / mu; return m * m / (2.0 * mu); }
+    *dv = -y;
+    return 1.0 - z - 0.5 * mu;
 }
 
 /* f_eval (objectives.py:129-133); target = b (primal) */
@@ -194,6 +205,11 @@ double or_f_eval(int kind, double lam, const double *target, const double *v, in
         }
         return 0.5 * acc;
     }
+    if (kind == 8) {            /* restated: sum smoothed hinge */
+        double g;
+        for (int64_t r = 0; r < d; ++r) acc += smooth_hinge(target[r], v[r], &g);
+        return acc;
+    }
     for (int64_t r = 0; r < d; ++r) {
         double e = v[r] - target[r];
         acc += e * e;
@@ -212,7 +228,8 @@ void or_f_grad(int kind, double lam, const double *target, const double *v, int6
         else if (kind == 7) {
             double m = 1.0 - target[r] * v[r];
             grad[r] = m > 0 ? -target[r] * m : 0.0;
-        } else grad[r] = v[r] - target[r];
+        } else if (kind == 8) smooth_hinge(target[r], v[r], &grad[r]);
+        else grad[r] = v[r] - target[r];
     }
 }
 
@@ -234,6 +251,14 @@ double or_f_conj(int kind, double lam, const double *target, const double *w, in
         for (int64_t r = 0; r < d; ++r) {
             double q = -w[r] * target[r];
             acc += 0.5 * q * q - q;
+        }
+        return acc;
+    }
+    if (kind == 8) {            /* h*(u) = u + mu u^2 / 2 on [-1, 0], u = y w */
+        for (int64_t r = 0; r < d; ++r) {
+            const double y = target[r] > 0.0 ? 1.0 : -1.0, mu = 1.0 / fabs(target[r]);
+            const double u = y * w[r];
+            acc += u + 0.5 * mu * u * u;
         }
         return acc;
     }
@@ -281,7 +306,7 @@ int or_step_from_ga(int kind, double lam, double rho, double y, double ga, doubl
                     double t, double *step) {
     if (!isfinite(ga)) return OR_SOLVER_ERROR;
     switch (kind) {
-    case 2: case 6: case 7:   /* ridge-type g = lam a^2/2 */
+    case 2: case 6: case 7: case 8:   /* ridge-type g = lam a^2/2 */
         *step = -(ga + lam * t) / (c + lam);
         return OR_OK;
     case 3:

@@ -154,7 +154,8 @@ __device__ __forceinline__ double g_one(int kind, double lam, double rho, double
     case GLM_DUAL_L2_SVM: return -a;
     case GLM_RIDGE_PRIMAL:
     case GLM_LOGISTIC_PRIMAL:
-    case GLM_SQUARED_HINGE_PRIMAL: return 0.5 * lam * a * a;
+    case GLM_SQUARED_HINGE_PRIMAL:
+    case GLM_HINGE_PRIMAL: return 0.5 * lam * a * a;
     case GLM_LASSO_PRIMAL: return lam * fabs(a);
     case GLM_DUAL_RIDGE: return 0.5 * a * a - y * a;
     case GLM_ELASTIC_NET_PRIMAL: return lam * (rho * fabs(a) + 0.5 * (1.0 - rho) * a * a);
@@ -169,7 +170,8 @@ __device__ __forceinline__ double g_conj_one(int kind, double lam, double rho, d
     case GLM_DUAL_L2_SVM: return fmax(0.0, s + 1.0);
     case GLM_RIDGE_PRIMAL:
     case GLM_LOGISTIC_PRIMAL:
-    case GLM_SQUARED_HINGE_PRIMAL: return s * s / (2.0 * lam);
+    case GLM_SQUARED_HINGE_PRIMAL:
+    case GLM_HINGE_PRIMAL: return s * s / (2.0 * lam);
     case GLM_DUAL_RIDGE: { double u = s + y; return 0.5 * u * u; }
     case GLM_ELASTIC_NET_PRIMAL: {
         if (rho >= 1.0) return NAN;
@@ -189,6 +191,7 @@ __device__ __forceinline__ bool coord_step(int kind, double lam, double rho, dou
     case GLM_RIDGE_PRIMAL:
     case GLM_LOGISTIC_PRIMAL:
     case GLM_SQUARED_HINGE_PRIMAL:
+    case GLM_HINGE_PRIMAL:
         step = -(ga + lam * t) / (c + lam);
         return true;
     case GLM_ELASTIC_NET_PRIMAL:
@@ -234,6 +237,12 @@ __device__ __forceinline__ bool coord_step(int kind, double lam, double rho, dou
 }
 
 // f contributions per row r (objectives.py:129-139, 205-208)
+// f(v) accumulated as squares and halved once at the end (quadratic kinds),
+// or as the per-row values themselves (logistic, smoothed hinge)
+__device__ __forceinline__ bool f_halved(int kind) {
+    return kind != GLM_LOGISTIC_PRIMAL && kind != GLM_HINGE_PRIMAL;
+}
+
 __device__ __forceinline__ void f_terms(int kind, double lam, double tgt, double v, double &f,
                                         double &g) {
     if (kind_is_dual(kind)) { f = v * v / (2.0 * lam); g = v / lam; return; }
@@ -248,6 +257,21 @@ __device__ __forceinline__ void f_terms(int kind, double lam, double tgt, double
         g = m > 0.0 ? -tgt * m : 0.0;
         return;
     }
+    if (kind == GLM_HINGE_PRIMAL) {      // smoothed hinge; the row target is y / mu
+        const double y = tgt > 0.0 ? 1.0 : -1.0, mu = 1.0 / fabs(tgt), z = y * v;
+        if (z >= 1.0) {
+            f = 0.0;
+            g = 0.0;
+        } else if (z > 1.0 - mu) {
+            const double m = 1.0 - z;
+            f = m * m / (2.0 * mu);
+            g = -y * m / mu;
+        } else {
+            f = 1.0 - z - 0.5 * mu;
+            g = -y;
+        }
+        return;
+    }
     double e = v - tgt;
     f = 0.5 * e * e;
     g = e;
@@ -257,6 +281,10 @@ __device__ __forceinline__ double f_conj_term(int kind, double lam, double tgt, 
     if (kind_is_dual(kind)) return 0.5 * lam * w * w;
     if (kind == GLM_LOGISTIC_PRIMAL) return entropy(-w * tgt);
     if (kind == GLM_SQUARED_HINGE_PRIMAL) { double q = -w * tgt; return 0.5 * q * q - q; }
+    if (kind == GLM_HINGE_PRIMAL) {      // h*(u) = u + mu u^2 / 2 on [-1, 0], u = y w
+        const double u = (tgt > 0.0 ? 1.0 : -1.0) * w, mu = 1.0 / fabs(tgt);
+        return u + 0.5 * mu * u * u;
+    }
     return 0.5 * w * w + w * tgt;
 }
 

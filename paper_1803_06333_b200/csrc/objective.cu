@@ -79,6 +79,11 @@ __global__ void __launch_bounds__(RED_THREADS) fgrad_kernel(int kind, double lam
             const double y = tgt[r];
             acc[0] += softplus(-y * x);
             if (grad) grad[r] = -y * sigmoid_tanh(-y * x);
+        } else if (kind == GLM_HINGE_PRIMAL) {
+            double f, g;
+            f_terms(kind, lam, tgt[r], x, f, g);
+            acc[0] += f;
+            if (grad) grad[r] = g;
         } else if (kind == GLM_SQUARED_HINGE_PRIMAL) {
             const double y = tgt[r], mg = 1.0 - y * x;
             acc[0] += mg > 0.0 ? mg * mg : 0.0;
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(RED_THREADS) fgrad_kernel(int kind, double lam
     if (reduce_last<1>(acc, scratch)) {
         double f = acc[0];
         if (dual) f = f / (2.0 * lam);
-        else if (kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+        else if (f_halved(kind)) f = 0.5 * f;
         *out_fv = f;
     }
 }
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(RED_THREADS) outer_model_kernel(int kind, doub
             g = x / lam;
         } else {
             f_terms(kind, lam, tgt[r], x, f, g);
-            if (kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;   // raw square, halved below
+            if (f_halved(kind)) f *= 2.0;   // raw square, halved below
         }
         acc[0] += f;
         grad[r] = g;
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(RED_THREADS) outer_model_kernel(int kind, doub
     if (reduce_last<1>(acc, scratch)) {
         double f = acc[0];
         if (dual) f = f / (2.0 * lam);
-        else if (kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+        else if (f_halved(kind)) f = 0.5 * f;
         *out_fv = f;
         *cnst = (f / K + 0.0) / L;   // ((fv/K) + grad.0 + 0)/L as engine.py:156-162
     }

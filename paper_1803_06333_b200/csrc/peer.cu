@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
             g = x / p.lam;
         } else {
             f_terms(p.kind, p.lam, p.tgt[r], x, f, g);
-            if (p.kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;
+            if (f_halved(p.kind)) f *= 2.0;
         }
         acc[0] += f;
         p.grad[r] = g;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
     if (!reduce_last<1>(acc, p.scratch)) return;
     double f = acc[0];
     if (dual) f = f / (2.0 * p.lam);
-    else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+    else if (f_halved(p.kind)) f = 0.5 * f;
     *p.out_fv = f;
     const double cn = (f / p.K + 0.0) / p.L;
     *p.cnst = cn;
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
                 f = vr * vr;
             } else {
                 f_terms(p.kind, p.lam, p.tgt[r], vr, f, g);
-                if (p.kind != GLM_LOGISTIC_PRIMAL) f *= 2.0;
+                if (f_halved(p.kind)) f *= 2.0;
             }
             acc[0] += f;
             if (active) {
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
                 st->block_counter = 0;
                 double f = t4[0];                       // round_start_kernel's scaling
                 if (kind_is_dual(p.kind)) f = f / (2.0 * p.lam);
-                else if (p.kind != GLM_LOGISTIC_PRIMAL) f = 0.5 * f;
+                else if (f_halved(p.kind)) f = 0.5 * f;
                 const double cn = (f / p.K + 0.0) / p.L;
                 *p.out_fv = f;
                 *p.cnst = cn;

@@ -461,6 +461,232 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
     store_block_gsum(gacc, p.gpart, st);
 }
 
+// Asynchronous narrow kernel, second form.  Two changes against scd_replica:
+//  * the shared view is published into REPLICA_COPIES copies (CTA b adds to
+//    copy b % K with a returning atomic and reads the other copies): the
+//    per-phase atomics of all CTAs no longer queue on d addresses
+//    (grid / K instead of grid same-address adds per row and phase);
+//  * each warp keeps REPLICA_DEPTH coordinates' columns and metadata in
+//    flight through a shared-memory ring filled by cp.async, the permutation
+//    entries twice as far ahead — the epoch streams 2.5 GB, and one column
+//    ahead per warp left only ~0.7 MB of loads in flight.
+// Same staleness budget and phase structure (per_phase coordinates per warp,
+// then fold + publish, the returns consumed one phase later).
+constexpr int REPLICA_COPIES = 8;
+// ring depth: 8 columns ahead for d <= 32, fewer for wider columns (smem)
+__host__ __device__ constexpr int replica_depth(int R) { return R <= 1 ? 8 : (R == 2 ? 4 : 2); }
+constexpr int REPLICA_WARPS = 8;
+constexpr int REPLICA_ROWS = 256;                // row stride between copies
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void narrow_pad2_kernel(const SolveState *st, const double *view0, const double *view1,
+                                   double *vpad, int64_t d, int64_t seq) {
+    if (skip_attempt(st, seq)) return;
+    const double *view = st->vw ? view1 : view0;
+    for (int64_t i = threadIdx.x; i < (int64_t)REPLICA_COPIES * d; i += blockDim.x) {
+        const int64_t c = i / d, r = i % d;
+        vpad[(c * REPLICA_ROWS + r) * PAD_STRIDE] = c == 0 ? view[r] : 0.0;
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p, int per_phase,
+                                                                   double *vpad) {
+    SolveState *st = p.st;
+    if (skip_attempt(st, p.seq)) return;
+    constexpr int SLOT = 32 * R + 4;                 // column + (b, dj, s, y)
+    constexpr int REPLICA_DEPTH = replica_depth(R);
+    __shared__ double snap[32 * R];
+    __shared__ double fold[32 * R];
+    __shared__ double ring[REPLICA_WARPS][REPLICA_DEPTH][SLOT];
+    __shared__ int jring[REPLICA_WARPS][REPLICA_DEPTH];
+    __shared__ int pring[REPLICA_WARPS][2 * REPLICA_DEPTH];
+    __shared__ int s_last;
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
+    double *view = st->vw ? p.view1 : p.view0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t d = p.d;
+    const int own = blockIdx.x % REPLICA_COPIES;
+    for (int r = threadIdx.x; r < 32 * R; r += blockDim.x) {
+        double x = 0.0;
+        if (r < d)
+            for (int c = 0; c < REPLICA_COPIES; ++c)
+                x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
+        snap[r] = x;
+        fold[r] = 0.0;
+    }
+    const int64_t per_cta = (int64_t)REPLICA_WARPS * per_phase;
+    const int64_t stride = (int64_t)gridDim.x * per_cta;
+    const int64_t kbase = (int64_t)blockIdx.x * per_cta + (int64_t)warp * per_phase;
+    // position t of this warp -> coordinate index k (increasing in t):
+    // k = kbase + (t / per_phase) * stride + t % per_phase, advanced without
+    // divisions (inside a phase k + 1, at its end the same slot of the next)
+    struct Pos {
+        int64_t k;
+        int i;
+    };
+    auto adv = [&](Pos q) -> Pos {
+        return q.i + 1 < per_phase ? Pos{q.k + 1, q.i + 1} : Pos{q.k - q.i + stride, 0};
+    };
+    double(*wring)[SLOT] = ring[warp];
+    auto issue = [&](int64_t t, int64_t k) {         // column + metadata of position t
+        const int slot = (int)(t % REPLICA_DEPTH);
+        if (k < p.m) {
+            const int j = pring[warp][t % (2 * REPLICA_DEPTH)];
+            const double *col = p.vals + (int64_t)j * d;
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (lane + 32 * i < d) cp_async8(&wring[slot][lane + 32 * i], col + lane + 32 * i);
+            if (lane == 0) {
+                cp_async8(&wring[slot][32 * R + 0], p.base + j);
+                cp_async8(&wring[slot][32 * R + 2], p.sq + j);
+                jring[warp][slot] = j;
+            } else if (lane == 1) {
+                if (dcur) cp_async8(&wring[slot][32 * R + 1], dcur + j);
+                else wring[slot][32 * R + 1] = 0.0;
+            } else if (lane == 2) {
+                if (p.y) cp_async8(&wring[slot][32 * R + 3], p.y + j);
+                else wring[slot][32 * R + 3] = 0.0;
+            }
+        }
+    };
+    auto issue_perm = [&](int64_t t, int64_t k) {
+        if (lane == 0 && k < p.m) {
+            const unsigned sa =
+                (unsigned)__cvta_generic_to_shared(&pring[warp][t % (2 * REPLICA_DEPTH)]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(p.perm + k)
+                         : "memory");
+        }
+    };
+    // prologue: permutation entries 0 .. 2D-1 (plain loads), columns 0 .. D-1
+    Pos q0{kbase, 0};                                // positions t, t + D, t + 2D
+    Pos qa = q0, qb;
+    for (int t = 0; t < 2 * REPLICA_DEPTH; ++t) {
+        if (lane == t) pring[warp][t] = qa.k < p.m ? __ldg(p.perm + qa.k) : 0;
+        if (t == REPLICA_DEPTH - 1) qb = adv(qa);
+        qa = adv(qa);
+    }
+    Pos q2 = qa;                                     // position 2D
+    __syncwarp();
+    {
+        Pos qi = q0;
+        for (int t = 0; t < REPLICA_DEPTH; ++t) {
+            issue(t, qi.k);
+            cp_async_commit();
+            qi = adv(qi);
+        }
+    }
+    Pos q1 = qb;                                     // position D
+    __syncthreads();
+    const int kind = p.kind;
+    double gacc = 0.0;
+    double pend[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) pend[i] = 0.0;
+    double prev_own = 0.0, prev_x = 0.0, prev_oth[REPLICA_COPIES];
+#pragma unroll
+    for (int c = 0; c < REPLICA_COPIES; ++c) prev_oth[c] = 0.0;
+    bool have_prev = false;
+    int64_t t = 0;
+    for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m; k0 += stride) {
+        for (int ii = 0; ii < per_phase; ++ii, ++t) {
+            if (q0.k >= p.m) break;
+            cp_async_wait<REPLICA_DEPTH - 1>();
+            __syncwarp();
+            const int slot = (int)(t % REPLICA_DEPTH);
+            double a[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i) a[i] = lane + 32 * i < d ? wring[slot][lane + 32 * i] : 0.0;
+            const double b = wring[slot][32 * R + 0], dj = wring[slot][32 * R + 1];
+            const double sj = wring[slot][32 * R + 2], yj = wring[slot][32 * R + 3];
+            const int j = jring[warp][slot];
+            __syncwarp();
+            issue(t + REPLICA_DEPTH, q1.k);           // reuses this slot
+            issue_perm(t + 2 * REPLICA_DEPTH, q2.k);
+            cp_async_commit();
+            q0 = adv(q0);
+            q1 = adv(q1);
+            q2 = adv(q2);
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) acc += a[i] * (snap[lane + 32 * i] + pend[i]);
+            const double ga = warp_allsum(acc);
+            double raw = 0.0;
+            if (!coord_step(kind, p.lam, p.rho, yj, ga, p.quad * sj, b + dj, raw)) {
+                if (lane == 0) flag_error(st);
+                raw = 0.0;
+            }
+            const double step = damping * raw;
+            const double dn = step != 0.0 ? dj + step : dj;
+            if (lane == 0) {
+                dnext[j] = dn;
+                gacc += g_one(kind, p.lam, p.rho, yj, b + dn);
+            }
+            if (step != 0.0) {
+                const double f = p.quad * step;
+#pragma unroll
+                for (int i = 0; i < R; ++i) pend[i] += f * a[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (pend[i] != 0.0) atomicAdd(&fold[lane + 32 * i], pend[i]);
+        __syncthreads();
+        if (threadIdx.x < d) {
+            const int r = threadIdx.x;
+            const double x = fold[r];
+            fold[r] = 0.0;
+            if (have_prev) {
+                double v = prev_own + prev_x;
+#pragma unroll
+                for (int c = 0; c < REPLICA_COPIES; ++c)
+                    if (c != own) v += prev_oth[c];
+                snap[r] = v + x;
+            } else {
+                snap[r] += x;
+            }
+            prev_own = atomicAdd(vpad + ((int64_t)own * REPLICA_ROWS + r) * PAD_STRIDE, x);
+#pragma unroll
+            for (int c = 0; c < REPLICA_COPIES; ++c)
+                if (c != own) prev_oth[c] = ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
+            prev_x = x;
+            have_prev = true;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) pend[i] = 0.0;
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    // the last CTA to finish writes the shared view back (copies in order)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&st->block_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int r = threadIdx.x; r < d; r += blockDim.x) {
+            double x = 0.0;
+            for (int c = 0; c < REPLICA_COPIES; ++c)
+                x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
+            view[r] = x;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) st->block_counter = 0;
+    }
+    store_block_gsum(gacc, p.gpart, st);
+}
+
 // ----------------------------------------------------------- sequential
 // One CTA of BS threads walks the permutation in order (run_pass with
 // n_threads=1, solver.py:202-211).  Deterministic: fixed per-thread strides
@@ -651,6 +877,299 @@ __global__ void __launch_bounds__(32) scd_seq_csc(EpochParams p) {
         for (int64_t r = lane; r < p.d; r += 32) gview[r] = sview[r];
     }
     if (lane == 0) {
+        p.gpart[0] = gacc;
+        st->epoch_blocks = 1;
+    }
+}
+
+// ------------------------------------------- sequential, level-scheduled
+// The deterministic epoch with the same bits as scd_seq_csc, but with many
+// coordinates in flight.  Coordinates whose columns share no row commute
+// exactly: the later one's gather does not see the earlier one's scatter.  So
+// a window of consecutive permutation entries is cut into levels — a
+// coordinate's level is one more than the highest level of an EARLIER window
+// entry it shares a row with — and the levels run one after another, each
+// level's coordinates concurrently.  Every coordinate then gathers exactly
+// the view the sequential walk would have shown it, and every row receives
+// the same writes in the same order, so view, delta and the epoch's g-sum
+// (summed afterwards in permutation order) are bit-identical to scd_seq_csc.
+//
+// Warp 0 plans window w+1 (permutation entries, column bounds, rows staged
+// through shared memory with cp.async, levels from a shared row -> level+1
+// table, cleared again right after the window is planned) while warps
+// 1..NW execute window w.
+constexpr int LVL_THREADS = 512;
+constexpr int LVL_WORKERS = LVL_THREADS / 32 - 1;
+constexpr int LVL_WINDOW = 256;
+constexpr int LVL_MAX = 31;                      // levels 0..30 per window
+constexpr int LVL_STAGE = 64;                    // staged rows per planned column
+constexpr int64_t LVL_TAB_MAX = 128 * 1024;      // rows with an in-smem level table
+constexpr int64_t LVL_SMEM_VIEW_MAX = 8 * 1024;  // doubles kept in shared memory
+constexpr size_t LVL_STAGE_BYTES = sizeof(uint32_t) * LVL_WINDOW * LVL_STAGE;
+
+struct LvlPlan {
+    int64_t lo[LVL_WINDOW];
+    int j[LVL_WINDOW];
+    int cnt[LVL_WINDOW];
+    double gterm[LVL_WINDOW];
+    uint16_t order[LVL_WINDOW];
+    uint8_t lvl[LVL_WINDOW];
+    uint16_t lstart[LVL_MAX + 1];
+    int n, nlev;
+    int64_t k0;
+};
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void workers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"r"(LVL_WORKERS * 32) : "memory");
+}
+
+// Warp 0: plan the window of permutation entries starting at k0.  The
+// window's permutation entries and column bounds are loaded with every load
+// in flight, its rows (up to LVL_STAGE per column) staged into shared memory
+// with cp.async, then the entries get their levels one after another from
+// the row -> level+1 table, which is cleared again from the staged rows.
+__device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *tab,
+                         uint32_t (*stage)[LVL_STAGE]) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rem = p.m - k0;
+    const int nmax = rem < LVL_WINDOW ? (int)rem : LVL_WINDOW;
+    constexpr int U = LVL_WINDOW / 32;
+    int jj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int c = u * 32 + lane;
+        jj[u] = c < nmax ? __ldg(p.perm + k0 + c) : 0;
+    }
+    int64_t lo[U], hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int c = u * 32 + lane;
+        lo[u] = c < nmax ? __ldg(p.indptr + jj[u]) : 0;
+        hi[u] = c < nmax ? __ldg(p.indptr + jj[u] + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int c = u * 32 + lane;
+        if (c < nmax) {
+            P.j[c] = jj[u];
+            P.lo[c] = lo[u];
+            P.cnt[c] = (int)(hi[u] - lo[u]);
+        }
+    }
+    __syncwarp();
+    for (int c = 0; c < nmax; ++c) {
+        const int64_t li = P.lo[c];
+        const int ci = P.cnt[c] < LVL_STAGE ? P.cnt[c] : LVL_STAGE;
+#pragma unroll
+        for (int r = 0; r < LVL_STAGE / 32; ++r)
+            if (lane + 32 * r < ci) cp_async4(&stage[c][lane + 32 * r], p.rows + li + lane + 32 * r);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // levels, one entry after another: the chain per entry is the table
+    // reads, one redux.sync max and the table writes (the entry's staged rows
+    // are read into registers one entry ahead)
+    int n = 0, maxlev = -1;
+    int r0n = 0, r1n = 0;
+    auto rows_of = [&](int c, int &r0, int &r1) {
+        const int ci = P.cnt[c];
+        r0 = lane < ci ? (int)stage[c][lane] : -1;
+        r1 = lane + 32 < ci && lane + 32 < LVL_STAGE ? (int)stage[c][lane + 32] : -1;
+    };
+    if (nmax > 0) rows_of(0, r0n, r1n);
+    for (int c = 0; c < nmax; ++c) {
+        const int r0 = r0n, r1 = r1n;
+        const int ci = P.cnt[c];
+        if (c + 1 < nmax) rows_of(c + 1, r0n, r1n);
+        int lv = -1;
+        if (r0 >= 0) lv = (int)tab[r0] - 1;
+        if (r1 >= 0) lv = max(lv, (int)tab[r1] - 1);
+        for (int q = LVL_STAGE + lane; q < ci; q += 32) lv = max(lv, (int)tab[__ldg(p.rows + P.lo[c] + q)] - 1);
+        const int level = __reduce_max_sync(0xffffffffu, lv) + 1;
+        if (level >= LVL_MAX) break;       // the window closes before this entry
+        if (r0 >= 0) tab[r0] = (uint8_t)(level + 1);
+        if (r1 >= 0) tab[r1] = (uint8_t)(level + 1);
+        for (int q = LVL_STAGE + lane; q < ci; q += 32) tab[__ldg(p.rows + P.lo[c] + q)] = (uint8_t)(level + 1);
+        if (lane == 0) P.lvl[c] = (uint8_t)level;
+        maxlev = max(maxlev, level);
+        n = c + 1;
+        __syncwarp();
+    }
+    __syncwarp();
+    // the table only serves dependencies inside a window: clear this one's rows
+    for (int c = 0; c < n; ++c) {
+        const int ci = P.cnt[c];
+        for (int q = lane; q < ci; q += 32)
+            tab[q < LVL_STAGE ? (int)stage[c][q] : __ldg(p.rows + P.lo[c] + q)] = 0;
+    }
+    __syncwarp();
+    // stable counting sort of the window's entries by level
+    const int nlev = maxlev + 1;
+    int base = 0;
+    for (int L = 0; L < nlev; ++L) {
+        if (lane == 0) P.lstart[L] = (uint16_t)base;
+        for (int c0 = 0; c0 < n; c0 += 32) {
+            const int c = c0 + lane;
+            const bool hit = c < n && P.lvl[c] == L;
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (hit) P.order[base + __popc(bal & ((1u << lane) - 1))] = (uint16_t)c;
+            base += __popc(bal);
+        }
+    }
+    if (lane == 0) {
+        P.lstart[nlev] = (uint16_t)base;
+        P.n = n;
+        P.nlev = nlev;
+        P.k0 = k0;
+    }
+    __syncwarp();
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
+    SolveState *st = p.st;
+    if (skip_attempt(st, p.seq)) return;
+    extern __shared__ __align__(16) unsigned char lvl_smem[];
+    __shared__ LvlPlan plans[2];
+    // dynamic: [staged rows of the planned window][view (SMEM)][row table]
+    uint32_t(*stage)[LVL_STAGE] = reinterpret_cast<uint32_t(*)[LVL_STAGE]>(lvl_smem);
+    double *sview = reinterpret_cast<double *>(lvl_smem + LVL_STAGE_BYTES);
+    uint8_t *tab = lvl_smem + LVL_STAGE_BYTES + (SMEM ? sizeof(double) * ((p.d + 1) & ~1LL) : 0);
+    const int dc = st->dc;
+    const double damping = st->damping;
+    const double *dcur = delta_cur(p, dc);
+    double *dnext = delta_next(p, dc);
+    double *gview = st->vw ? p.view1 : p.view0;
+    double *V = SMEM ? sview : gview;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t r = threadIdx.x; r < p.d; r += blockDim.x) {
+        if (SMEM) sview[r] = gview[r];
+        tab[r] = 0;
+    }
+    __syncthreads();
+    if (warp == 0) lvl_plan(p, plans[0], 0, tab, stage);
+    __syncthreads();
+    const int kind = p.kind;
+    double gacc = 0.0;
+    struct Col {
+        int j, cnt, slot;
+        int64_t lo;
+        int rows[3];
+        double vals[3];
+        double b, dj, s, y;
+    };
+    for (int w = 0;; ++w) {
+        LvlPlan &P = plans[w & 1];
+        const int n = P.n;
+        if (n == 0) {
+            if (threadIdx.x == 0 && w > 0) {     // the last window's g terms
+                const LvlPlan &Q = plans[(w - 1) & 1];
+                for (int c = 0; c < Q.n; ++c) gacc += Q.gterm[c];
+            }
+            break;
+        }
+        if (warp == 0) {
+            // the previous window's g terms, in permutation order (scd_seq_csc's sum)
+            if (w > 0 && lane == 0) {
+                const LvlPlan &Q = plans[(w - 1) & 1];
+                for (int c = 0; c < Q.n; ++c) gacc += Q.gterm[c];
+            }
+            __syncwarp();
+            const int64_t k1 = P.k0 + n;
+            if (k1 < p.m) lvl_plan(p, plans[(w + 1) & 1], k1, tab, stage);
+            else if (lane == 0) plans[(w + 1) & 1].n = 0;
+        } else {
+            const int me = warp - 1;
+            auto load = [&](int e, Col &c) {
+                const int slot = P.order[e];
+                c.slot = slot;
+                c.j = P.j[slot];
+                c.lo = P.lo[slot];
+                c.cnt = P.cnt[slot];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const bool in = lane + 32 * i < c.cnt;
+                    c.rows[i] = in ? __ldg(p.rows + c.lo + lane + 32 * i) : 0;
+                    c.vals[i] = in ? __ldg(p.vals + c.lo + lane + 32 * i) : 0.0;
+                }
+                c.b = __ldg(p.base + c.j);
+                c.dj = dcur ? dcur[c.j] : 0.0;
+                c.s = __ldg(p.sq + c.j);
+                c.y = p.y ? __ldg(p.y + c.j) : 0.0;
+            };
+            // this worker's entries, level after level; the next one's column
+            // (independent of the view) is loaded before the current one steps
+            const int nlev = P.nlev;
+            int L = 0;
+            int e = P.lstart[0] + me;
+            auto advance = [&](int &e_, int &L_) {      // next own entry, possibly a later level
+                while (L_ < nlev && e_ >= P.lstart[L_ + 1]) {
+                    ++L_;
+                    if (L_ < nlev) e_ = P.lstart[L_] + me;
+                }
+            };
+            advance(e, L);
+            Col nx;
+            if (L < nlev) load(e, nx);
+            int cur_level = 0;
+            while (L < nlev) {
+                while (cur_level < L) {      // levels this worker has nothing in
+                    workers_sync();
+                    ++cur_level;
+                }
+                const Col c = nx;
+                int e2 = e + LVL_WORKERS, L2 = L;
+                advance(e2, L2);
+                if (L2 < nlev) load(e2, nx);
+                double g[3];
+                double acc = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    g[i] = lane + 32 * i < c.cnt ? V[c.rows[i]] : 0.0;
+                    if (lane + 32 * i < c.cnt) acc += c.vals[i] * g[i];
+                }
+                for (int q = lane + 96; q < c.cnt; q += 32) acc += p.vals[c.lo + q] * V[p.rows[c.lo + q]];
+                acc = warp_sum(acc);
+                double raw = 0.0;
+                if (!coord_step(kind, p.lam, p.rho, c.y, acc, p.quad * c.s, c.b + c.dj, raw)) {
+                    if (lane == 0) flag_error(st);
+                    raw = 0.0;
+                }
+                const double step = damping * raw;
+                const double dn = step != 0.0 ? c.dj + step : c.dj;
+                if (lane == 0) {
+                    dnext[c.j] = dn;
+                    P.gterm[c.slot] = g_one(kind, p.lam, p.rho, c.y, c.b + dn);
+                }
+                if (step != 0.0) {
+                    const double f = p.quad * step;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        if (lane + 32 * i < c.cnt) V[c.rows[i]] = g[i] + f * c.vals[i];
+                    for (int q = lane + 96; q < c.cnt; q += 32) V[p.rows[c.lo + q]] += f * p.vals[c.lo + q];
+                }
+                __syncwarp();
+                e = e2;
+                L = L2;
+            }
+            while (cur_level < nlev) {       // the barriers of the remaining levels
+                workers_sync();
+                ++cur_level;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (SMEM)
+        for (int64_t r = threadIdx.x; r < p.d; r += blockDim.x) gview[r] = sview[r];
+    if (threadIdx.x == 0) {
         p.gpart[0] = gacc;
         st->epoch_blocks = 1;
     }
@@ -967,6 +1486,12 @@ static int narrow_rows(int64_t d) {
     return 0;
 }
 
+// GLM_NARROW_KERNEL=v1: the single-copy, one-ahead narrow async kernel
+static bool narrow_v1_forced() {
+    const char *e = getenv("GLM_NARROW_KERNEL");
+    return e && strcmp(e, "v1") == 0;
+}
+
 template <int R>
 static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, double *vpad,
                            cudaStream_t s) {
@@ -974,14 +1499,21 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, dou
     if (!async) {
         scd_seq_narrow<R><<<1, 32, 0, s>>>(p);
     } else {
-        static int blocks_per_sm = 0;
+        static int blocks_per_sm = 0, blocks_per_sm2 = 0;
         if (!blocks_per_sm) {
             GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
                                                                        scd_replica<R>, 256, 0));
             if (blocks_per_sm < 1) blocks_per_sm = 1;
         }
+        const bool v1 = narrow_v1_forced();
+        if (!v1 && !blocks_per_sm2) {
+            GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &blocks_per_sm2, scd_replica2<R>, 32 * REPLICA_WARPS, 0));
+            if (blocks_per_sm2 < 1) blocks_per_sm2 = 1;
+        }
         constexpr int W = 8;
-        int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
+        static_assert(W == REPLICA_WARPS, "one warp count for both narrow kernels");
+        int64_t cap = (int64_t)(v1 ? blocks_per_sm : blocks_per_sm2) * NUM_SMS;
         if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
         int64_t grid = budget / W;
         if (grid < 1) grid = 1;
@@ -991,9 +1523,15 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, dou
         int64_t per = budget / (grid * W);
         if (per < 1) per = 1;
         if (per > 64) per = 64;
-        narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
-        count_launch();
-        scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+        if (v1) {
+            narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
+            count_launch();
+            scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+        } else {
+            narrow_pad2_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
+            count_launch();
+            scd_replica2<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+        }
     }
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
@@ -1048,8 +1586,35 @@ static int64_t narrow_budget(const EpochParams &p, double sq_mean, int max_infli
 
 constexpr int64_t SMEM_VIEW_MAX = 24 * 1024;   // doubles (192 KB)
 
+// GLM_SEQ_KERNEL=csc keeps the one-warp walk (A/B checks of the level-
+// scheduled kernel, which must produce the same bits)
+static bool seq_csc_forced() {
+    const char *e = getenv("GLM_SEQ_KERNEL");
+    return e && strcmp(e, "csc") == 0;
+}
+
 template <int BS, bool DENSE>
 static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
+    if (BS == 32 && !DENSE && p.d <= LVL_TAB_MAX && !seq_csc_forced()) {
+        const bool sv = p.d <= LVL_SMEM_VIEW_MAX;
+        const size_t tab = (size_t)((p.d + 16) & ~15LL);
+        const size_t bytes =
+            LVL_STAGE_BYTES + tab + (sv ? sizeof(double) * (size_t)((p.d + 1) & ~1LL) : 0);
+        count_launch();
+        if (sv) {
+            GLM_CUDA_TRY(cudaFuncSetAttribute(scd_seq_lvl<true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)bytes));
+            scd_seq_lvl<true><<<1, LVL_THREADS, bytes, s>>>(p);
+        } else {
+            GLM_CUDA_TRY(cudaFuncSetAttribute(scd_seq_lvl<false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)bytes));
+            scd_seq_lvl<false><<<1, LVL_THREADS, bytes, s>>>(p);
+        }
+        GLM_CUDA_TRY(cudaGetLastError());
+        return GLM_OK;
+    }
     if (BS == 32 && !DENSE) {   // short CSC columns: the pipelined one-warp kernel
         if (p.d <= SMEM_VIEW_MAX) {
             size_t bytes = sizeof(double) * (size_t)(p.d > 0 ? p.d : 1);
@@ -1206,7 +1771,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     if (m > s->max_coords || d > s->max_rows)
         return glm_set_error(GLM_USAGE, "partition larger than the solver was created for");
     if (m >= (1LL << 31)) return glm_set_error(GLM_USAGE, "partition exceeds 2^31 coordinates");
-    if (a->kind < 0 || a->kind > GLM_SQUARED_HINGE_PRIMAL)
+    if (a->kind < 0 || a->kind > GLM_HINGE_PRIMAL)
         return glm_set_error(GLM_USAGE, "unknown objective kind");
     if (!(a->quad > 0.0)) return glm_set_error(GLM_USAGE, "quad must be positive");
     if (a->kind == GLM_DUAL_RIDGE && !a->coord_target)

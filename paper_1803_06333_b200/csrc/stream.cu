@@ -502,7 +502,7 @@ int glm_stream_solve(glm_stream *S, const glm_stream_args *a, double *damping_io
     if (!S || !a || !a->lin || !a->base || !damping_io || !delta_io)
         return glm_set_error(GLM_USAGE, "null argument to glm_stream_solve");
     if (a->epochs < 1) return glm_set_error(GLM_USAGE, "t_epochs must be >= 1");
-    if (a->kind < 0 || a->kind > GLM_SQUARED_HINGE_PRIMAL)
+    if (a->kind < 0 || a->kind > GLM_HINGE_PRIMAL)
         return glm_set_error(GLM_USAGE, "unknown objective kind");
     if (!(a->quad > 0.0)) return glm_set_error(GLM_USAGE, "quad must be positive");
     if (a->kind == GLM_DUAL_RIDGE && !a->coord_target)

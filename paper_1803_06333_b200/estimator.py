@@ -34,11 +34,13 @@ OBJECTIVE_NAMES = {
     "elastic-net": "elastic_net_primal",
     "logistic": "logistic_primal",
     "squared-hinge": "squared_hinge_primal",
+    "hinge": "hinge_primal",
 }
-CLASSIFIERS = ("dual_l2_logistic", "dual_l2_svm", "logistic_primal", "squared_hinge_primal")
+CLASSIFIERS = ("dual_l2_logistic", "dual_l2_svm", "logistic_primal", "squared_hinge_primal",
+               "hinge_primal")
 
 _DEFAULTS = dict(objective="dual-logistic", lam=1.0, devices=1, t2=1, epochs=2, threads=1,
-                 seed=0, max_rounds=20, target_gap=None, l1_ratio=1.0)
+                 seed=0, max_rounds=20, target_gap=None, l1_ratio=1.0, smoothing=1.0)
 
 
 class NotFittedError(ValueError, AttributeError):
@@ -112,7 +114,8 @@ class GlmEstimator:
     Parameters mirror EstimatorParams (estimator.ts:20-40): objective, lam
     (lambda), devices (L), t2, epochs, threads (threads per device: 1 runs the
     deterministic sequential kernel, > 1 the asynchronous TPA-SCD kernel),
-    seed, max_rounds, target_gap; l1_ratio for elastic-net.
+    seed, max_rounds, target_gap; l1_ratio for elastic-net; smoothing (mu) for
+    the smoothed hinge-loss SVM (objective "hinge").
     """
 
     def __init__(self, **params):
@@ -179,7 +182,7 @@ class GlmEstimator:
         else:
             matrix = ex.transpose()
             spec = ObjectiveSpec(kind, p["lam"], matrix.n_rows, matrix.n_cols, target=y,
-                                 l1_ratio=p["l1_ratio"])
+                                 l1_ratio=p["l1_ratio"], smoothing=p["smoothing"])
         cfg = HierarchyConfig(nodes=1, devices=p["devices"], t1=p["max_rounds"], t2=p["t2"],
                               epochs=p["epochs"], threads_per_device=p["threads"],
                               seed=p["seed"])

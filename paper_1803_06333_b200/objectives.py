@@ -6,7 +6,7 @@ with the same names, constants and error behaviour. The arithmetic
 csrc/objective.cu; the functions here are host entry points that take numpy
 or device arrays.
 
-Kinds 0..3 are the reference's (objectives.py:22). Kinds 4..7 are restated
+Kinds 0..3 are the reference's (objectives.py:22). Kinds 4..8 are restated
 kinds the north star names but the reference does not implement (parity
 unpinned):
 
@@ -14,6 +14,11 @@ unpinned):
   elastic_net_primal    f(v) = ||v - b||^2/2,   g_i(a) = lam (rho|a| + (1-rho) a^2/2)
   logistic_primal       f(v) = sum softplus(-y v), g_i(a) = lam a^2/2, beta = 1/4
   squared_hinge_primal  f(v) = 1/2 sum max(0, 1 - y v)^2, g_i(a) = lam a^2/2
+  hinge_primal          f(v) = sum h_mu(y v), g_i(a) = lam a^2/2, beta = 1/mu: the
+                        hinge loss smoothed over a width mu = `smoothing`
+                        (h_mu(z) = 0 for z >= 1, (1-z)^2/(2 mu) above 1 - mu,
+                        1 - z - mu/2 below); mu -> 0 is the hinge-loss SVM.
+                        The device kernels read its row target as y / mu.
 """
 
 from __future__ import annotations
@@ -24,7 +29,8 @@ from dataclasses import dataclass
 import numpy as np
 
 KINDS = ("dual_l2_logistic", "dual_l2_svm", "ridge_primal", "lasso_primal",
-         "dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal")
+         "dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal",
+         "hinge_primal")
 REFERENCE_KINDS = KINDS[:4]
 
 BOUNDARY_EPS = 1e-12  # objectives.py:26
@@ -39,7 +45,8 @@ class ObjectiveSpec:
     """Objective selection plus the constants the rate bounds need
     (objectives.py:39-112). `target` is b for primal kinds (length = rows),
     and the per-example label/response y for logistic_primal,
-    squared_hinge_primal and dual_ridge. `l1_ratio` is elastic-net rho."""
+    squared_hinge_primal, hinge_primal and dual_ridge. `l1_ratio` is
+    elastic-net rho; `smoothing` is the hinge_primal smoothing width mu."""
 
     kind: str
     lam: float
@@ -47,6 +54,7 @@ class ObjectiveSpec:
     n_features: int
     target: np.ndarray | None = None
     l1_ratio: float = 1.0
+    smoothing: float = 1.0
 
     def __post_init__(self):
         if self.kind not in KINDS:
@@ -54,11 +62,14 @@ class ObjectiveSpec:
         if self.lam <= 0:
             raise ValueError("lambda must be positive")
         if self.kind in ("ridge_primal", "lasso_primal", "elastic_net_primal",
-                         "logistic_primal", "squared_hinge_primal", "dual_ridge") \
+                         "logistic_primal", "squared_hinge_primal", "hinge_primal",
+                         "dual_ridge") \
                 and self.target is None:
             raise ValueError(f"{self.kind} requires a target vector")
         if self.kind == "elastic_net_primal" and not (0.0 <= self.l1_ratio <= 1.0):
             raise ValueError("l1_ratio must lie in [0, 1]")
+        if self.kind == "hinge_primal" and not self.smoothing > 0.0:
+            raise ValueError("smoothing must be positive")
 
     @property
     def index(self) -> int:
@@ -82,13 +93,16 @@ class ObjectiveSpec:
     def beta(self):
         if self.is_dual:
             return 1.0 / self.lam
+        if self.kind == "hinge_primal":
+            return 1.0 / self.smoothing
         return 0.25 if self.kind == "logistic_primal" else 1.0
 
     @property
     def mu(self):
         if self.kind == "dual_l2_logistic":
             return 4.0
-        if self.kind in ("ridge_primal", "logistic_primal", "squared_hinge_primal"):
+        if self.kind in ("ridge_primal", "logistic_primal", "squared_hinge_primal",
+                         "hinge_primal"):
             return self.lam
         if self.kind == "dual_ridge":
             return 1.0
@@ -109,8 +123,14 @@ class ObjectiveSpec:
 
     @property
     def row_target(self):
-        """Vector indexed by rows of A (b or y per example) or None."""
-        return None if (self.is_dual or self.target is None) else self.target
+        """Vector indexed by rows of A (b or y per example) or None; for
+        hinge_primal y / mu (the kernels take the label from its sign and the
+        smoothing width from its magnitude)."""
+        if self.is_dual or self.target is None:
+            return None
+        if self.kind == "hinge_primal":
+            return np.asarray(self.target, dtype=np.float64) / self.smoothing
+        return self.target
 
     @property
     def coord_target(self):

@@ -421,7 +421,7 @@ class _CtxCache:
 
 _KIND_INDEX = {"dual_l2_logistic": 0, "dual_l2_svm": 1, "ridge_primal": 2, "lasso_primal": 3,
                "dual_ridge": 4, "elastic_net_primal": 5, "logistic_primal": 6,
-               "squared_hinge_primal": 7}
+               "squared_hinge_primal": 7, "hinge_primal": 8}
 
 
 def device_solve_host(ctx, sub, gen_state, damping, epochs, mode, out=None):

@@ -27,6 +27,9 @@ def _problem(kind, seed=0, n=300, d=40, k=6):
     elif kind == "elastic_net_primal":
         cols, tgt = X, X @ rng.standard_normal(d) + 0.1 * rng.standard_normal(n)
         spec = g.ObjectiveSpec(kind, 2.0, n, d, target=tgt, l1_ratio=0.6)
+    elif kind == "hinge_primal":
+        cols, tgt = X, y
+        spec = g.ObjectiveSpec(kind, 1.2, n, d, target=tgt, smoothing=0.25)
     else:
         cols, tgt = X, y
         spec = g.ObjectiveSpec(kind, 1.2, n, d, target=tgt)
@@ -37,7 +40,8 @@ def _problem(kind, seed=0, n=300, d=40, k=6):
     return m, spec
 
 
-KINDS = ["dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal"]
+KINDS = ["dual_ridge", "elastic_net_primal", "logistic_primal", "squared_hinge_primal",
+         "hinge_primal"]
 
 
 @pytest.mark.parametrize("kind", KINDS)

@@ -63,7 +63,14 @@ def test_objective_constants_table():
 def test_objective_spec_errors():
     from paper_1803_06333_b200.objectives import UnsupportedObjectiveError
     with pytest.raises(UnsupportedObjectiveError):
+        g.ObjectiveSpec("hinge_loss_svm", 1.0, 2, 2)
+    with pytest.raises(ValueError, match="requires a target"):
         g.ObjectiveSpec("hinge_primal", 1.0, 2, 2)
+    with pytest.raises(ValueError, match="smoothing"):
+        g.ObjectiveSpec("hinge_primal", 1.0, 2, 2, target=np.ones(2), smoothing=0.0)
+    hs = g.ObjectiveSpec("hinge_primal", 1.0, 2, 2, target=np.array([1.0, -1.0]), smoothing=0.25)
+    assert hs.beta == 4.0 and hs.has_gap
+    np.testing.assert_array_equal(hs.row_target, [4.0, -4.0])
     with pytest.raises(ValueError):
         g.ObjectiveSpec("ridge_primal", 1.0, 2, 2)
     with pytest.raises(ValueError):

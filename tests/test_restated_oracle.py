@@ -106,6 +106,63 @@ def test_squared_hinge_primal_matches_lbfgs():
     assert r["gap"][-1] < 1e-8
 
 
+def _hinge_problem():
+    X, rng = _examples(240, 12, 5, 9)
+    y = np.where(X @ rng.standard_normal(12) + 0.2 * rng.standard_normal(240) >= 0, 1.0, -1.0)
+    return X, y
+
+
+@pytest.mark.parametrize("mu", [1.0, 0.3])
+def test_smoothed_hinge_primal_matches_lbfgs(mu):
+    """hinge_primal (smoothed hinge of width mu; the oracle's target is y / mu)
+    against L-BFGS on the same smooth objective, with a certified gap."""
+    X, y = _hinge_problem()
+    lam = 0.5
+    A = _csc_of(X)
+    r = oracle.train(A, "hinge_primal", lam, target=y / mu, rounds=4000, epochs=2, seed=8)
+
+    def fg(w):
+        z = y * (X @ w)
+        h = np.where(z >= 1, 0.0, np.where(z > 1 - mu, (1 - z) ** 2 / (2 * mu), 1 - z - mu / 2))
+        dh = np.where(z >= 1, 0.0, np.where(z > 1 - mu, -(1 - z) / mu, -1.0))
+        return 0.5 * lam * w @ w + h.sum(), lam * w + X.T @ (y * dh)
+
+    ref = optimize.minimize(fg, np.zeros(12), jac=True, method="L-BFGS-B",
+                            options={"maxiter": 20000, "ftol": 1e-15, "gtol": 1e-12})
+    assert r["objective"][-1] == pytest.approx(ref.fun, rel=1e-8)
+    np.testing.assert_allclose(r["alpha"], ref.x, atol=1e-4)
+    assert r["gap"][-1] < 1e-9 * abs(r["objective"][-1])
+    assert np.all(np.diff(r["objective"]) <= 1e-12 * abs(r["objective"][0]))
+
+
+def test_smoothed_hinge_tends_to_the_hinge_svm():
+    """mu -> 0 is the hinge-loss SVM.  Its optimum comes from the reference
+    kind dual_l2_svm on the label-folded examples (a certified gap < 1e-8:
+    hinge* = -F_dual*); the hinge objective of the smoothed solution lies in
+    [hinge*, hinge* + n mu / 2 + its certified gap], a bracket that closes as
+    mu shrinks."""
+    X, y = _hinge_problem()
+    lam = 0.5
+    Ad = _csc_of((X * y[:, None]).T)
+    rd = oracle.train(Ad, "dual_l2_svm", lam, rounds=3000, epochs=2, seed=8)
+    assert rd["gap"][-1] < 1e-8
+    hinge_star = -rd["objective"][-1]
+    A = _csc_of(X)
+
+    def hinge_obj(w):
+        return 0.5 * lam * w @ w + np.maximum(0.0, 1.0 - y * (X @ w)).sum()
+
+    # the primal of the dual solution is the hinge optimum itself
+    assert hinge_obj(rd["v"] / lam) == pytest.approx(hinge_star, rel=1e-7)
+    excess = []
+    for mu in (1.0, 0.3, 0.1):
+        r = oracle.train(A, "hinge_primal", lam, target=y / mu, rounds=4000, epochs=2, seed=8)
+        f_mu = hinge_obj(r["alpha"])
+        assert hinge_star - 1e-7 <= f_mu <= hinge_star + 0.5 * len(y) * mu + r["gap"][-1], mu
+        excess.append(f_mu - hinge_star)
+    assert excess[0] > excess[1] > excess[2]
+
+
 def test_restated_steps_minimise_their_1d_models():
     rng = np.random.default_rng(7)
     for _ in range(200):
