@@ -412,13 +412,15 @@ def train(m, kind, lam, *, target=None, nodes=1, devices=1, t2=1, epochs=1, seed
 
     t0 = time.perf_counter()
     gap = record()
-    if target_rel_gap is not None:
-        target_gap = target_rel_gap * abs(objs[0])
     pool = ThreadPoolExecutor(max_workers=K * L) if parallel else None
     done = 0
     round_s = []
     for _ in range(rounds):
         if target_gap is not None and gap is not None and gap <= target_gap:
+            break
+        # relative target: gap <= rel * |F| of the current round (bench.py's bar)
+        if target_rel_gap is not None and gap is not None and \
+                gap <= target_rel_gap * abs(objs[-1]):
             break
         tr = time.perf_counter()
         grad = f_grad(k, lam, target, v)                   # engine.py:271

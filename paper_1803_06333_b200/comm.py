@@ -187,6 +187,19 @@ class NcclReducer:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
+    def allgather(self, t):
+        """Every rank's tensor, in rank order (the parts of canonical_sum)."""
+        if self._aborted:
+            raise ReduceError("collective aborted")
+        if self.staged:
+            h = t.cpu()
+            got = [torch.empty_like(h) for _ in range(self.world)]
+            dist.all_gather(got, h, group=self.group)
+            return [g.to(t.device) for g in got]
+        flat = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(flat, t.contiguous(), group=self.group)
+        return list(flat.view(self.world, -1))
+
     def broadcast(self, vec):
         t, was_tensor = self._tensor(vec)
         t = t.clone()

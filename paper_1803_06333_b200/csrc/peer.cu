@@ -32,16 +32,22 @@
 struct glm_peer {
     int device = 0, rank = 0, world = 1;
     int64_t d = 0;
-    // [ctl: 8 x i64 | flag slots: world x i64 | pad to 256 B | dv: 2 x d doubles]
+    // [ctl: 16 x i64 | flag slots: 24 x i64 | reduced-flag slots: 24 x i64 | pad to
+    //  PEER_HEADER B | dv: 2 x pstride doubles | reduced slice sums: 2 x pstride doubles]
     char *mem = nullptr;
     int64_t *ctl = nullptr;       // [0] published rounds, [1] consumed, [2] block counter,
                                   // [3] "every rank published" (turn), [4] their accept
                                   // bits, [5] our last flag word, [6] round-start ticket,
-                                  // [7] error word (a wait that timed out)
+                                  // [7] error word (a wait that timed out), [8] reduce-
+                                  // scatter arrivals, [9] "every rank reduced" (turn)
     int64_t *flags = nullptr;     // local slots: flags[j] = rank j's last flag word
     double *dv = nullptr;         // 2 halves of pstride doubles (Delta v[d], padded)
     int64_t pstride = 0;
     double **bufs_dev = nullptr;  // world pointers to each rank's dv (device array)
+    double **red_dev = nullptr;   // world pointers to each rank's reduced slice sums
+    int64_t *flags2 = nullptr;    // local reduced-flag slots
+    int64_t **flags2_dev = nullptr;  // world pointers to each rank's reduced-flag slots
+    int rs = 0;                   // turn P3 as reduce-scatter + all-gather
     int64_t **flags_dev = nullptr;  // world pointers to each rank's flag slots
     std::vector<void *> opened;   // cudaIpc-opened peer allocations
     uint64_t *stamps = nullptr;   // glm_peer_stamps: turn phase timestamps (debug)
@@ -54,7 +60,9 @@ namespace glm {
 
 constexpr int PEER_BLOCKS = 2 * NUM_SMS;
 constexpr int PEER_THREADS = 256;
-constexpr int PEER_MAX_WORLD = 24;      // flag slots that fit the 256-byte header
+constexpr int PEER_MAX_WORLD = 24;      // flag slots per array in the header
+constexpr int PEER_HEADER = 512;        // ctl[16] + flags[24] + flags2[24] doubles-aligned
+constexpr int PEER_FLAGS = 16, PEER_FLAGS2 = 40;   // i64 offsets of the flag arrays
 
 // doubles per parity half: Delta v[d] padded to 256 B
 inline int64_t peer_pstride(int64_t d) { return ((d > 0 ? d : 1) + 1 + 31) / 32 * 32; }
@@ -145,6 +153,20 @@ __device__ __forceinline__ uint32_t wait_flags(const int64_t *flags, int world, 
         if (!late) mask |= (uint32_t)((f >> (R & 1)) & 1) << j;
     }
     return mask;
+}
+
+// Every local reduced-flag slot at round >= R (one thread), with the deadline.
+__device__ __forceinline__ void wait_rounds(const int64_t *flags, int world, int64_t R,
+                                            int64_t *ctl, uint64_t timeout) {
+    uint64_t t0 = 0;
+    for (int j = 0; j < world; ++j)
+        while (ld_acquire_sys(flags + j) < R) {
+            __nanosleep(32);
+            if (expired(t0, timeout)) {
+                peer_fail(ctl, PEER_ERR_FLAGS, j);
+                break;
+            }
+        }
 }
 
 // Finalize of a solve whose Delta v goes to the peer exchange: alpha += delta
@@ -422,6 +444,11 @@ struct TurnParams {
     double *scratch;
     uint64_t *stamps;          // optional phase timestamps (globaltimer ns)
     uint64_t timeout;          // deadline of every wait (ns)
+    int rs;                    // P3 as reduce-scatter + all-gather
+    double *red_own;           // this rank's reduced slice sums (2 parity halves)
+    double *const *red;        // every rank's reduced slice sums
+    int64_t *const *flags2;    // every rank's reduced-flag slots
+    const int64_t *flags2_in;  // local reduced-flag slots
 };
 
 
@@ -621,8 +648,44 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     const int64_t off = (R & 1) * p.pstride;
     const uint32_t accm = s_acc;
     const bool dual = kind_is_dual(p.kind);
+    // Reduce-scatter + all-gather (3+ ranks): rank j sums, in rank order, only
+    // its slice [j cs, (j+1) cs) of every rank's Delta v and publishes it; every
+    // rank then reads each row's sum from the slice owner — (N-1)/N * 8d bytes
+    // read twice instead of (N-1) * 8d, the same rank-order sum per row.
+    const int64_t cs = (p.d + (int64_t)p.world * 32 - 1) / ((int64_t)p.world * 32) * 32;
+    if (p.rs) {
+        const int64_t lo = (int64_t)p.rank * cs, hi = lo + cs < p.d ? lo + cs : p.d;
+        for (int64_t r = lo + tid; r < hi; r += nth)
+            p.red_own[off + r] = rank_sum(p.bufs, p.world, off + r, accm);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const bool last = atomicAdd(reinterpret_cast<unsigned long long *>(p.ctl + 8), 1ull) ==
+                              (unsigned long long)(gridDim.x - 1);
+            if (last) {                // every block's slice rows are written: publish
+                p.ctl[8] = 0;
+                __threadfence_system();
+                for (int j = 0; j < p.world; ++j) st_relaxed_sys(p.flags2[j] + p.rank, R);
+            }
+            if (blockIdx.x == 0) {
+                wait_rounds(p.flags2_in, p.world, R, p.ctl, p.timeout);
+                __threadfence();
+                atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 9), (unsigned long long)R);
+            } else {
+                uint64_t t0 = 0;
+                while ((int64_t)ld_acquire_gpu_u64(p.ctl + 9) < R) {
+                    __nanosleep(32);
+                    if (expired(t0, 2 * p.timeout)) {
+                        peer_fail(p.ctl, PEER_ERR_GRID, 5);
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
     for (int64_t r = tid; r < p.d; r += nth) {
-        const double s = rank_sum(p.bufs, p.world, off + r, accm);
+        const double s = p.rs ? __ldcg(p.red[r / cs] + off + r) : rank_sum(p.bufs, p.world, off + r, accm);
         const double x = p.v[r] + s;
         p.v[r] = x;
         double f, g;
@@ -703,6 +766,8 @@ int glm_peer_destroy(glm_peer *p) {
     cudaFree(p->mem);
     cudaFree(p->bufs_dev);
     cudaFree(p->flags_dev);
+    cudaFree(p->red_dev);
+    cudaFree(p->flags2_dev);
     cudaSetDevice(prev);
     delete p;
     return GLM_OK;
@@ -720,11 +785,13 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
     p->world = world;
     p->d = d;
     p->pstride = peer_pstride(d);
-    const size_t bytes = 256 + sizeof(double) * 2 * (size_t)p->pstride;
+    const size_t bytes = PEER_HEADER + sizeof(double) * 4 * (size_t)p->pstride;
     cudaError_t e = cudaMalloc(&p->mem, bytes);
     if (e == cudaSuccess) e = cudaMemset(p->mem, 0, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->bufs_dev, sizeof(double *) * world);
     if (e == cudaSuccess) e = cudaMalloc(&p->flags_dev, sizeof(int64_t *) * world);
+    if (e == cudaSuccess) e = cudaMalloc(&p->red_dev, sizeof(double *) * world);
+    if (e == cudaSuccess) e = cudaMalloc(&p->flags2_dev, sizeof(int64_t *) * world);
     if (e == cudaSuccess && world > 1) e = cudaIpcGetMemHandle(&p->handle, p->mem);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -746,13 +813,22 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
     p->turn_blocks = (occ < 2 ? occ : 2) * sms;
     if (p->turn_blocks > PEER_BLOCKS) p->turn_blocks = PEER_BLOCKS;
     p->ctl = reinterpret_cast<int64_t *>(p->mem);
-    p->dv = reinterpret_cast<double *>(p->mem + 256);
-    p->flags = p->ctl + 8;
+    p->dv = reinterpret_cast<double *>(p->mem + PEER_HEADER);
+    p->flags = p->ctl + PEER_FLAGS;
+    p->flags2 = p->ctl + PEER_FLAGS2;
+    // reduce-scatter + all-gather once there are 3+ ranks (at 2 it moves the
+    // same bytes as reading the peer's whole Delta v, plus a flag round trip);
+    // GLM_PEER_RS=0/1 overrides
+    p->rs = world >= 3;
+    if (const char *env = getenv("GLM_PEER_RS")) p->rs = env[0] == '1';
     if (world == 1) {
-        double *b = p->dv;
-        int64_t *f = p->flags;
+        p->rs = 0;
+        double *b = p->dv, *rd = p->dv + 2 * p->pstride;
+        int64_t *f = p->flags, *f2 = p->flags2;
         GLM_CUDA_TRY(cudaMemcpy(p->bufs_dev, &b, sizeof(b), cudaMemcpyHostToDevice));
         GLM_CUDA_TRY(cudaMemcpy(p->flags_dev, &f, sizeof(f), cudaMemcpyHostToDevice));
+        GLM_CUDA_TRY(cudaMemcpy(p->red_dev, &rd, sizeof(rd), cudaMemcpyHostToDevice));
+        GLM_CUDA_TRY(cudaMemcpy(p->flags2_dev, &f2, sizeof(f2), cudaMemcpyHostToDevice));
     }
     *out = p;
     return GLM_OK;
@@ -771,8 +847,8 @@ int glm_peer_open(glm_peer *p, const void *handles) {
     if (p->world == 1) return GLM_OK;
     if (!handles) return glm_set_error(GLM_USAGE, "world > 1 needs every rank's handle");
     GLM_CUDA_TRY(cudaSetDevice(p->device));
-    std::vector<double *> bufs(p->world);
-    std::vector<int64_t *> flags(p->world);
+    std::vector<double *> bufs(p->world), red(p->world);
+    std::vector<int64_t *> flags(p->world), flags2(p->world);
     for (int j = 0; j < p->world; ++j) {
         char *base;
         if (j == p->rank) {
@@ -785,12 +861,18 @@ int glm_peer_open(glm_peer *p, const void *handles) {
             p->opened.push_back(q);
             base = (char *)q;
         }
-        flags[j] = reinterpret_cast<int64_t *>(base) + 8;
-        bufs[j] = reinterpret_cast<double *>(base + 256);
+        flags[j] = reinterpret_cast<int64_t *>(base) + PEER_FLAGS;
+        flags2[j] = reinterpret_cast<int64_t *>(base) + PEER_FLAGS2;
+        bufs[j] = reinterpret_cast<double *>(base + PEER_HEADER);
+        red[j] = bufs[j] + 2 * p->pstride;
     }
     GLM_CUDA_TRY(cudaMemcpy(p->bufs_dev, bufs.data(), sizeof(double *) * p->world,
                             cudaMemcpyHostToDevice));
     GLM_CUDA_TRY(cudaMemcpy(p->flags_dev, flags.data(), sizeof(int64_t *) * p->world,
+                            cudaMemcpyHostToDevice));
+    GLM_CUDA_TRY(cudaMemcpy(p->red_dev, red.data(), sizeof(double *) * p->world,
+                            cudaMemcpyHostToDevice));
+    GLM_CUDA_TRY(cudaMemcpy(p->flags2_dev, flags2.data(), sizeof(int64_t *) * p->world,
                             cudaMemcpyHostToDevice));
     return GLM_OK;
 }
@@ -919,6 +1001,11 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
     a.scratch = scratch;
     a.stamps = p->stamps;
     a.timeout = p->timeout_ns;
+    a.rs = p->rs;
+    a.red_own = p->dv + 2 * p->pstride;
+    a.red = p->red_dev;
+    a.flags2 = p->flags2_dev;
+    a.flags2_in = p->flags2;
     cudaStream_t st = (cudaStream_t)stream;
     if (s->timing) {
         int rc = glue_begin(s, 2, st);

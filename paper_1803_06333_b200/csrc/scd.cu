@@ -41,6 +41,8 @@
 // SpMV (the reference recomputes it exactly, solver.py:300); the parity tests
 // bound the difference (tests/test_gpu_solver.py).
 
+#include <cstdio>
+
 #include "solver.cuh"
 
 namespace glm {
@@ -346,7 +348,8 @@ __global__ void narrow_pad_kernel(const SolveState *st, const double *view0, con
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase, double *vpad) {
+__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase, double *vpad,
+                                                   int delay2) {
     SolveState *st = p.st;
     if (skip_attempt(st, p.seq)) return;
     __shared__ double snap[32 * R];
@@ -371,8 +374,11 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
     const int64_t per_cta = (int64_t)nwarp * per_phase;
     const int64_t stride = (int64_t)gridDim.x * per_cta;
-    double prev_old = 0.0, prev_x = 0.0;   // row threadIdx.x: the last publish
-    bool have_prev = false;
+    // row threadIdx.x: the publishes still in flight.  With delay 2 the atomic's
+    // return is consumed two phases later (its round trip spans two phases);
+    // the snapshot is then old(p-2) + x(p-2) + x(p-1) + x(p).
+    double prev_old = 0.0, prev_x = 0.0, prev2_old = 0.0, prev2_x = 0.0;
+    int published = 0;
     // This warp's coordinates: position t -> k(t) = base + (t / P) * stride +
     // t % P.  Two-stage software pipeline: the permutation entry of t + 2 and
     // the column of t + 1 are in flight while t is stepped (the column load
@@ -436,10 +442,16 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
             const int r = threadIdx.x;
             const double x = fold[r];
             fold[r] = 0.0;
-            snap[r] = have_prev ? prev_old + prev_x + x : snap[r] + x;
+            if (delay2) {
+                snap[r] = published >= 2 ? prev2_old + prev2_x + prev_x + x : snap[r] + x;
+                prev2_old = prev_old;
+                prev2_x = prev_x;
+            } else {
+                snap[r] = published >= 1 ? prev_old + prev_x + x : snap[r] + x;
+            }
             prev_old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
             prev_x = x;
-            have_prev = true;
+            ++published;
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) pend[i] = 0.0;
@@ -472,7 +484,7 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
 //    ahead per warp left only ~0.7 MB of loads in flight.
 // Same staleness budget and phase structure (per_phase coordinates per warp,
 // then fold + publish, the returns consumed one phase later).
-constexpr int REPLICA_COPIES = 8;
+constexpr int REPLICA_COPIES = 8;            // the most copies scd_replica2 spreads over
 // ring depth: 8 columns ahead for d <= 32, fewer for wider columns (smem)
 __host__ __device__ constexpr int replica_depth(int R) { return R <= 1 ? 8 : (R == 2 ? 4 : 2); }
 constexpr int REPLICA_WARPS = 8;
@@ -487,16 +499,16 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void narrow_pad2_kernel(const SolveState *st, const double *view0, const double *view1,
-                                   double *vpad, int64_t d, int64_t seq) {
+                                   double *vpad, int64_t d, int64_t seq, int copies) {
     if (skip_attempt(st, seq)) return;
     const double *view = st->vw ? view1 : view0;
-    for (int64_t i = threadIdx.x; i < (int64_t)REPLICA_COPIES * d; i += blockDim.x) {
+    for (int64_t i = threadIdx.x; i < (int64_t)copies * d; i += blockDim.x) {
         const int64_t c = i / d, r = i % d;
         vpad[(c * REPLICA_ROWS + r) * PAD_STRIDE] = c == 0 ? view[r] : 0.0;
     }
 }
 
-template <int R>
+template <int R, int C>
 __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p, int per_phase,
                                                                    double *vpad) {
     SolveState *st = p.st;
@@ -516,11 +528,11 @@ __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p
     double *view = st->vw ? p.view1 : p.view0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t d = p.d;
-    const int own = blockIdx.x % REPLICA_COPIES;
+    const int own = blockIdx.x % C;
     for (int r = threadIdx.x; r < 32 * R; r += blockDim.x) {
         double x = 0.0;
         if (r < d)
-            for (int c = 0; c < REPLICA_COPIES; ++c)
+            for (int c = 0; c < C; ++c)
                 x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
         snap[r] = x;
         fold[r] = 0.0;
@@ -593,9 +605,9 @@ __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p
     double pend[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
-    double prev_own = 0.0, prev_x = 0.0, prev_oth[REPLICA_COPIES];
+    double prev_own = 0.0, prev_x = 0.0, prev_oth[C];
 #pragma unroll
-    for (int c = 0; c < REPLICA_COPIES; ++c) prev_oth[c] = 0.0;
+    for (int c = 0; c < C; ++c) prev_oth[c] = 0.0;
     bool have_prev = false;
     int64_t t = 0;
     for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m; k0 += stride) {
@@ -649,7 +661,7 @@ __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p
             if (have_prev) {
                 double v = prev_own + prev_x;
 #pragma unroll
-                for (int c = 0; c < REPLICA_COPIES; ++c)
+                for (int c = 0; c < C; ++c)
                     if (c != own) v += prev_oth[c];
                 snap[r] = v + x;
             } else {
@@ -657,7 +669,7 @@ __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p
             }
             prev_own = atomicAdd(vpad + ((int64_t)own * REPLICA_ROWS + r) * PAD_STRIDE, x);
 #pragma unroll
-            for (int c = 0; c < REPLICA_COPIES; ++c)
+            for (int c = 0; c < C; ++c)
                 if (c != own) prev_oth[c] = ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
             prev_x = x;
             have_prev = true;
@@ -677,7 +689,7 @@ __global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p
         __threadfence();
         for (int r = threadIdx.x; r < d; r += blockDim.x) {
             double x = 0.0;
-            for (int c = 0; c < REPLICA_COPIES; ++c)
+            for (int c = 0; c < C; ++c)
                 x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
             view[r] = x;
         }
@@ -911,7 +923,8 @@ struct LvlPlan {
     int64_t lo[LVL_WINDOW];
     int j[LVL_WINDOW];
     int cnt[LVL_WINDOW];
-    double gterm[LVL_WINDOW];
+    double gterm[LVL_WINDOW];    // b + delta of the entry, then g(b + delta)
+    double gy[LVL_WINDOW];       // the entry's y (dual_ridge)
     uint16_t order[LVL_WINDOW];
     uint8_t lvl[LVL_WINDOW];
     uint16_t lstart[LVL_MAX + 1];
@@ -963,13 +976,13 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
             P.cnt[c] = (int)(hi[u] - lo[u]);
         }
     }
-    __syncwarp();
-    for (int c = 0; c < nmax; ++c) {
-        const int64_t li = P.lo[c];
-        const int ci = P.cnt[c] < LVL_STAGE ? P.cnt[c] : LVL_STAGE;
+    // stage the rows: lane l copies the columns l, l + 32, ... (bounds in registers)
 #pragma unroll
-        for (int r = 0; r < LVL_STAGE / 32; ++r)
-            if (lane + 32 * r < ci) cp_async4(&stage[c][lane + 32 * r], p.rows + li + lane + 32 * r);
+    for (int u = 0; u < U; ++u) {
+        const int c = u * 32 + lane;
+        const int64_t cu = hi[u] - lo[u];
+        const int ci = c < nmax ? (cu < LVL_STAGE ? (int)cu : LVL_STAGE) : 0;
+        for (int q = 0; q < ci; ++q) cp_async4(&stage[c][q], p.rows + lo[u] + q);
     }
     cp_async_wait_all();
     __syncwarp();
@@ -977,38 +990,58 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
     // reads, one redux.sync max and the table writes (the entry's staged rows
     // are read into registers one entry ahead)
     int n = 0, maxlev = -1;
-    int r0n = 0, r1n = 0;
-    auto rows_of = [&](int c, int &r0, int &r1) {
-        const int ci = P.cnt[c];
+    int r0n = 0, r1n = 0, cin = 0;
+    auto rows_of = [&](int c, int &r0, int &r1, int &ci) {
+        ci = P.cnt[c];
         r0 = lane < ci ? (int)stage[c][lane] : -1;
         r1 = lane + 32 < ci && lane + 32 < LVL_STAGE ? (int)stage[c][lane + 32] : -1;
     };
-    if (nmax > 0) rows_of(0, r0n, r1n);
+    bool longcols = false;
+    if (nmax > 0) rows_of(0, r0n, r1n, cin);
     for (int c = 0; c < nmax; ++c) {
-        const int r0 = r0n, r1 = r1n;
-        const int ci = P.cnt[c];
-        if (c + 1 < nmax) rows_of(c + 1, r0n, r1n);
+        const int r0 = r0n, r1 = r1n, ci = cin;
+        if (c + 1 < nmax) rows_of(c + 1, r0n, r1n, cin);
         int lv = -1;
         if (r0 >= 0) lv = (int)tab[r0] - 1;
         if (r1 >= 0) lv = max(lv, (int)tab[r1] - 1);
-        for (int q = LVL_STAGE + lane; q < ci; q += 32) lv = max(lv, (int)tab[__ldg(p.rows + P.lo[c] + q)] - 1);
+        if (ci > LVL_STAGE) {              // rows past the staged ones (rare)
+            longcols = true;
+            for (int q = LVL_STAGE + lane; q < ci; q += 32)
+                lv = max(lv, (int)tab[__ldg(p.rows + P.lo[c] + q)] - 1);
+        }
         const int level = __reduce_max_sync(0xffffffffu, lv) + 1;
         if (level >= LVL_MAX) break;       // the window closes before this entry
         if (r0 >= 0) tab[r0] = (uint8_t)(level + 1);
         if (r1 >= 0) tab[r1] = (uint8_t)(level + 1);
-        for (int q = LVL_STAGE + lane; q < ci; q += 32) tab[__ldg(p.rows + P.lo[c] + q)] = (uint8_t)(level + 1);
+        if (ci > LVL_STAGE)
+            for (int q = LVL_STAGE + lane; q < ci; q += 32)
+                tab[__ldg(p.rows + P.lo[c] + q)] = (uint8_t)(level + 1);
         if (lane == 0) P.lvl[c] = (uint8_t)level;
         maxlev = max(maxlev, level);
         n = c + 1;
         __syncwarp();
     }
     __syncwarp();
-    // the table only serves dependencies inside a window: clear this one's rows
-    for (int c = 0; c < n; ++c) {
-        const int ci = P.cnt[c];
-        for (int q = lane; q < ci; q += 32)
-            tab[q < LVL_STAGE ? (int)stage[c][q] : __ldg(p.rows + P.lo[c] + q)] = 0;
+    // the table only serves dependencies inside a window: clear this one's
+    // rows (eight entries' staged rows read before any is cleared)
+    for (int c0 = 0; c0 < n; c0 += 8) {
+        int ra[8], rb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = c0 + u;
+            const int ci = c < n ? P.cnt[c] : 0;
+            ra[u] = lane < ci ? (int)stage[c][lane] : -1;
+            rb[u] = lane + 32 < ci && lane + 32 < LVL_STAGE ? (int)stage[c][lane + 32] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (ra[u] >= 0) tab[ra[u]] = 0;
+            if (rb[u] >= 0) tab[rb[u]] = 0;
+        }
     }
+    if (__any_sync(0xffffffffu, longcols))
+        for (int c = 0; c < n; ++c)
+            for (int q = LVL_STAGE + lane; q < P.cnt[c]; q += 32) tab[__ldg(p.rows + P.lo[c] + q)] = 0;
     __syncwarp();
     // stable counting sort of the window's entries by level
     const int nlev = maxlev + 1;
@@ -1031,6 +1064,10 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
     }
     __syncwarp();
 }
+
+// GLM_LVL_DEBUG=1: the kernel prints where its time went (cycles of warp 0
+// planning and of worker warp 1 executing, windows, levels)
+__device__ int lvl_debug = 0;
 
 template <bool SMEM>
 __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
@@ -1065,23 +1102,29 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
         double vals[3];
         double b, dj, s, y;
     };
+    long long dbg_busy = 0, dbg_levels = 0, dbg_windows = 0;
+    const long long dbg_t0 = clock64();
     for (int w = 0;; ++w) {
         LvlPlan &P = plans[w & 1];
         const int n = P.n;
-        if (n == 0) {
-            if (threadIdx.x == 0 && w > 0) {     // the last window's g terms
-                const LvlPlan &Q = plans[(w - 1) & 1];
+        const long long dbg_w0 = clock64();
+        // the previous window's g terms: g(b + delta) evaluated lane-parallel
+        // off the workers' critical path, then summed in permutation order
+        // (scd_seq_csc's sum, the same bits)
+        auto window_gsum = [&](LvlPlan &Q) {
+            for (int c = lane; c < Q.n; c += 32)
+                Q.gterm[c] = g_one(kind, p.lam, p.rho, Q.gy[c], Q.gterm[c]);
+            __syncwarp();
+            if (lane == 0)
                 for (int c = 0; c < Q.n; ++c) gacc += Q.gterm[c];
-            }
+            __syncwarp();
+        };
+        if (n == 0) {
+            if (warp == 0 && w > 0) window_gsum(plans[(w - 1) & 1]);     // the last window
             break;
         }
         if (warp == 0) {
-            // the previous window's g terms, in permutation order (scd_seq_csc's sum)
-            if (w > 0 && lane == 0) {
-                const LvlPlan &Q = plans[(w - 1) & 1];
-                for (int c = 0; c < Q.n; ++c) gacc += Q.gterm[c];
-            }
-            __syncwarp();
+            if (w > 0) window_gsum(plans[(w - 1) & 1]);
             const int64_t k1 = P.k0 + n;
             if (k1 < p.m) lvl_plan(p, plans[(w + 1) & 1], k1, tab, stage);
             else if (lane == 0) plans[(w + 1) & 1].n = 0;
@@ -1144,16 +1187,17 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
                 }
                 const double step = damping * raw;
                 const double dn = step != 0.0 ? c.dj + step : c.dj;
-                if (lane == 0) {
-                    dnext[c.j] = dn;
-                    P.gterm[c.slot] = g_one(kind, p.lam, p.rho, c.y, c.b + dn);
-                }
-                if (step != 0.0) {
+                if (step != 0.0) {          // the scatter first: the next level waits on it
                     const double f = p.quad * step;
 #pragma unroll
                     for (int i = 0; i < 3; ++i)
                         if (lane + 32 * i < c.cnt) V[c.rows[i]] = g[i] + f * c.vals[i];
                     for (int q = lane + 96; q < c.cnt; q += 32) V[p.rows[c.lo + q]] += f * p.vals[c.lo + q];
+                }
+                if (lane == 0) {
+                    dnext[c.j] = dn;
+                    P.gterm[c.slot] = c.b + dn;     // g() applied by warp 0 after the window
+                    P.gy[c.slot] = c.y;
                 }
                 __syncwarp();
                 e = e2;
@@ -1163,9 +1207,15 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
                 workers_sync();
                 ++cur_level;
             }
+            dbg_levels += nlev;
         }
+        dbg_busy += clock64() - dbg_w0;
+        ++dbg_windows;
         __syncthreads();
     }
+    if (lvl_debug && lane == 0 && warp <= 1)
+        printf("scd_seq_lvl warp %d: busy %lld of %lld cycles, %lld windows, %lld levels\n", warp,
+               dbg_busy, clock64() - dbg_t0, dbg_windows, dbg_levels);
     __syncthreads();
     if (SMEM)
         for (int64_t r = threadIdx.x; r < p.d; r += blockDim.x) gview[r] = sview[r];
@@ -1486,10 +1536,21 @@ static int narrow_rows(int64_t d) {
     return 0;
 }
 
-// GLM_NARROW_KERNEL=v1: the single-copy, one-ahead narrow async kernel
+// GLM_NARROW_KERNEL=v2: the replicated-copies narrow kernel (slower: the
+// reads of the other copies cost more L2 requests than the atomics it spreads)
 static bool narrow_v1_forced() {
     const char *e = getenv("GLM_NARROW_KERNEL");
-    return e && strcmp(e, "v1") == 0;
+    return !(e && strcmp(e, "v2") == 0);
+}
+// GLM_NARROW_COPIES=8: scd_replica2 spreads the view over 8 copies (default 1)
+static int narrow_copies() {
+    const char *e = getenv("GLM_NARROW_COPIES");
+    return e && strcmp(e, "8") == 0 ? REPLICA_COPIES : 1;
+}
+// GLM_NARROW_DELAY=2: consume the publish's atomic return two phases later
+static int narrow_delay2() {
+    const char *e = getenv("GLM_NARROW_DELAY");
+    return e && strcmp(e, "2") == 0 ? 1 : 0;
 }
 
 template <int R>
@@ -1506,9 +1567,10 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, dou
             if (blocks_per_sm < 1) blocks_per_sm = 1;
         }
         const bool v1 = narrow_v1_forced();
+        const int copies = narrow_copies();
         if (!v1 && !blocks_per_sm2) {
             GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks_per_sm2, scd_replica2<R>, 32 * REPLICA_WARPS, 0));
+                &blocks_per_sm2, scd_replica2<R, 1>, 32 * REPLICA_WARPS, 0));
             if (blocks_per_sm2 < 1) blocks_per_sm2 = 1;
         }
         constexpr int W = 8;
@@ -1526,11 +1588,12 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, dou
         if (v1) {
             narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
             count_launch();
-            scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+            scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad, narrow_delay2());
         } else {
-            narrow_pad2_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
+            narrow_pad2_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq, copies);
             count_launch();
-            scd_replica2<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+            if (copies == 1) scd_replica2<R, 1><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
+            else scd_replica2<R, REPLICA_COPIES><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
         }
     }
     GLM_CUDA_TRY(cudaGetLastError());
@@ -1596,6 +1659,12 @@ static bool seq_csc_forced() {
 template <int BS, bool DENSE>
 static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
     if (BS == 32 && !DENSE && p.d <= LVL_TAB_MAX && !seq_csc_forced()) {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("GLM_LVL_DEBUG");
+            dbg = e && e[0] == '1';
+            if (dbg) GLM_CUDA_TRY(cudaMemcpyToSymbol(lvl_debug, &dbg, sizeof(int)));
+        }
         const bool sv = p.d <= LVL_SMEM_VIEW_MAX;
         const size_t tab = (size_t)((p.d + 16) & ~15LL);
         const size_t bytes =

@@ -15,7 +15,11 @@ round except the solve status; `record()` reads back 4 scalars (the trace).
 Topology: all K x L workers of a process share its GPU (virtual devices, used
 for parity with the reference's in-process engine), or — with a reducer and
 node_index — one process owns node `node_index` (one GPU per process, NCCL
-between processes).
+between processes), or — with device_index and a node_reducer as well — one
+process owns the single worker (node_index, device_index): the two-level
+scheme across GPUs, K x L ranks, each inner round folding the node's Delta v
+over the node's ranks (engine.py:259-266) and each outer round summing the
+nodes' v_bar over all ranks (engine.py:282).
 """
 
 from __future__ import annotations
@@ -174,7 +178,8 @@ class Engine:
     def __init__(self, matrix, spec, config, reducer=None, cost_model=None, node_index=None,
                  measure_theta_bar=False, measure_theta_outer=False, chunk_runner=None,
                  mode=None, sync_solves=True, retry_budget=2, group_lanes=0, max_inflight=0,
-                 n_total=None, cache_flags=0, peer_exchange=True, peer_timeout=None):
+                 n_total=None, cache_flags=0, peer_exchange=True, peer_timeout=None,
+                 device_index=None, node_reducer=None):
         if measure_theta_bar or measure_theta_outer:
             raise ValueError("theta measurement is the reference's CPU test-mode oracle "
                              "(solver.py:308-391); it is out of scope on the device path")
@@ -197,6 +202,12 @@ class Engine:
         self.max_inflight = int(max_inflight)
         self.cache_flags = int(cache_flags)
         local_input = isinstance(matrix, DeviceMatrix) and node_index is not None
+        if device_index is not None and node_index is None:
+            raise ValueError("device_index needs node_index (a rank owns one (node, device))")
+        if device_index is not None and config.devices > 1 and node_reducer is None:
+            raise ValueError("a rank per device needs the node's reducer (node_reducer)")
+        self.device_index = None if device_index is None else int(device_index)
+        self.node_reducer = node_reducer
         if local_input and n_total is None:
             raise ValueError("a node-local DeviceMatrix needs n_total (global coordinates)")
         n = int(n_total) if local_input else matrix.n_cols
@@ -219,16 +230,20 @@ class Engine:
         self.local_nodes = local_nodes
         self.node_index = node_index
         # device matrix: the whole matrix in-process, only the node's columns otherwise
-        if local_input:     # caller uploaded only node_index's columns
-            self.dm, self.col_offset = matrix, int(self.bounds[node_index * L_])
-            if matrix.n_cols != int(self.bounds[(node_index + 1) * L_]) - self.col_offset:
-                raise ValueError("local matrix does not match the node's partition")
+        if self.device_index is not None:      # this rank's worker columns only
+            w_lo = node_index * L_ + self.device_index
+            lo, hi = int(self.bounds[w_lo]), int(self.bounds[w_lo + 1])
+        elif node_index is not None:
+            lo, hi = int(self.bounds[node_index * L_]), int(self.bounds[(node_index + 1) * L_])
+        if local_input:     # caller uploaded only this rank's columns
+            self.dm, self.col_offset = matrix, lo
+            if matrix.n_cols != hi - lo:
+                raise ValueError("local matrix does not match the rank's partition")
         elif isinstance(matrix, DeviceMatrix):
             self.dm, self.col_offset = matrix, 0
         elif node_index is None:
             self.dm, self.col_offset = matrix.device(), 0
         else:
-            lo, hi = self.bounds[node_index * L_], self.bounds[(node_index + 1) * L_]
             sub = matrix.select_columns(np.arange(lo, hi)) if not hasattr(matrix, "dense") \
                 else None
             self.dm = sub.device() if sub is not None else \
@@ -238,7 +253,7 @@ class Engine:
         f = dict(dtype=torch.float64, device=self.device)
         self.workers = {}
         for k in local_nodes:
-            for l in range(L_):
+            for l in (range(L_) if self.device_index is None else [self.device_index]):
                 w = k * L_ + l
                 self.workers[(k, l)] = _Worker(self, k, l, self.bounds[w], self.bounds[w + 1],
                                                k * L_ + l)
@@ -428,7 +443,9 @@ class Engine:
         D = _D()
         L_ = cfg.devices
         qo = cfg.sigma_eff * self.spec.beta
-        wks = [self.workers[(k, l)] for l in range(L_)]
+        per_rank = self.device_index is not None
+        wks = [self.workers[(k, l)] for l in
+               ([self.device_index] if per_rank else range(L_))]
         for t in range(cfg.t2):
             if t > 0 or not self._lin_fresh:
                 # lin = grad + qo*vbar ; cnst = (fv/K + grad.vbar + qo/2|vbar|^2)/L
@@ -443,9 +460,27 @@ class Engine:
             # each result into v_bar as it lands keeps the reference's device-order
             # sum (engine.py:264-266) without a second pass
             self._lin_fresh = False
+            if per_rank:
+                # this rank's device solves into a zeroed Delta v; the node's
+                # ranks then fold every device's Delta v into v_bar in device
+                # order — the same additions, in the same order, as the
+                # in-process fold below (engine.py:264-266)
+                dv = self._dv_local()
+                self._solve_worker(wks[0], self.lin, cnst, first_inner=(t == 0), vbar=dv)
+                parts = self.node_reducer.allgather(dv) if L_ > 1 else [dv]
+                for part in parts:
+                    L.check(L.lib().glm_axpby(self.d, 1.0, D.ptr(part), 1.0, D.ptr(vbar),
+                                              D.sptr(self.stream)), "glm_axpby")
+                continue
             for wk in wks:                       # canonical device order
                 self._solve_worker(wk, self.lin, cnst, first_inner=(t == 0), vbar=vbar)
         return vbar
+
+    def _dv_local(self):
+        if getattr(self, "_dv_loc", None) is None:
+            self._dv_loc = torch.zeros(max(self.d, 1), dtype=torch.float64, device=self.device)
+        self._dv_loc.zero_()
+        return self._dv_loc
 
     def _outer_round_fused(self):
         """One round with the exchange over peer memory: glm_round_start applies
@@ -523,6 +558,8 @@ class Engine:
             else:
                 self.total.zero_()
                 self._run_node(self.local_nodes[0], self.total)
+                if self.device_index:          # one contribution per node (its device 0)
+                    self.total.zero_()
                 self.reducer.allreduce_inplace(self.total)   # engine.py:282
         except BaseException:
             if self.reducer is not None and hasattr(self.reducer, "abort"):

@@ -77,3 +77,59 @@ def test_gloo_two_rank_reducer_semantics():
         assert "mismatch" in o["mismatch"]
     assert res[0]["det"].tobytes() == res[1]["det"].tobytes()
     assert res[0]["part"] == (0, 500_000) and res[1]["part"] == (500_000, 1_000_000)
+
+
+def _hier_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_06333_b200.comm import NcclReducer
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, L = 2, 2
+        node, dev = divmod(rank, L)
+        groups = [dist.new_group(list(range(k * L, (k + 1) * L))) for k in range(K)]
+        node_red = NcclReducer(group=groups[node], deterministic=True)
+        glob = NcclReducer(deterministic=True)
+        rng = np.random.default_rng(5)
+        dvs = rng.standard_normal((2, K, L, 64)) * 1e3      # [inner round, node, device]
+        # Engine._run_node with one rank per device: v_bar += every device's
+        # Delta v in device order, then the outer sum with one contribution per node
+        vbar = torch.zeros(64, dtype=torch.float64)
+        for t in range(2):
+            for part in node_red.allgather(torch.from_numpy(dvs[t, node, dev].copy())):
+                vbar += part
+        total = vbar.clone() if dev == 0 else torch.zeros(64, dtype=torch.float64)
+        glob.allreduce_inplace(total)
+        q.put((rank, total.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_four_rank_hierarchical_fold():
+    """K = 2 nodes x L = 2 devices as four gloo ranks: the node fold over an
+    allgather plus the outer sum with one contribution per node equals the
+    in-process nested fold (engine.py:259-282) bit for bit."""
+    world = 4
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_hier_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dvs = np.random.default_rng(5).standard_normal((2, 2, 2, 64)) * 1e3
+    total = np.zeros(64)
+    for k in range(2):
+        vbar = np.zeros(64)
+        for t in range(2):
+            for l in range(2):
+                vbar = vbar + dvs[t, k, l]
+        total = total + vbar
+    for r in range(world):
+        assert res[r].tobytes() == total.tobytes()

@@ -81,6 +81,14 @@ def test_fused_round_reset_and_graph_replay():
     np.testing.assert_array_equal(eng.v, v_eager)
 
 
+def _why(out):
+    """The child's own traceback (torchrun's summary follows it on stderr)."""
+    err = out.stderr
+    i = err.find("Traceback (most recent call last)")
+    head = err[i:i + 4000] if i >= 0 else err[-3000:]
+    return out.stdout[-1500:] + "\n--- stderr ---\n" + head
+
+
 def _free_port():
     import socket
     sk = socket.socket()
@@ -90,32 +98,36 @@ def _free_port():
     return port
 
 
-def _torchrun(*extra, timeout=600):
+def _torchrun(*extra, timeout=600, script="mp_exchange_check.py", nproc=2, env=None):
     return subprocess.run(
-        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-         os.path.join(ROOT, "tests", "mp_exchange_check.py"), *extra],
-        capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+         f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+         "--master-port", str(_free_port()), os.path.join(ROOT, "tests", script), *extra],
+        capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+        env=None if env is None else dict(os.environ, **env))
 
 
 def test_two_process_exchange_matches_nccl():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     out = _torchrun()
-    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert out.returncode == 0, _why(out)
     assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
     assert "GRAPH async OK" in out.stdout, out.stdout[-2000:]
 
 
-def test_two_process_exchange_same_gpu():
+@pytest.mark.parametrize("rs", ["0", "1"])
+def test_two_process_exchange_same_gpu(rs):
     """Both ranks on cuda:0 (gloo bootstrap, time-sliced contexts): the IPC
     mappings, the pushed flag words, the parity double buffer and the
     rank-ordered sum of csrc/peer.cu across two processes, bit-identical to the
     deterministic reducer and to the in-process K = 2 engine; then the benched
     kernel configuration (async, cache_flags=1, fused turn) replayed from a
-    CUDA graph across the ranks, with v = A alpha afterwards."""
-    out = _torchrun("--same-gpu")
-    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    CUDA graph across the ranks, with v = A alpha afterwards.  rs = 1 runs the
+    turn's exchange as reduce-scatter + all-gather over peer memory (the
+    default from 3 ranks up): the same bits."""
+    out = _torchrun("--same-gpu", env={"GLM_PEER_RS": rs})
+    assert out.returncode == 0, _why(out)
     assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
     assert "GRAPH sequential OK" in out.stdout and "GRAPH async OK" in out.stdout, \
         out.stdout[-2000:]
@@ -129,3 +141,23 @@ def test_dead_rank_surfaces_as_error():
     assert "TIMEOUT OK" in out.stdout or "TIMEOUT CUDA" in out.stdout, \
         out.stdout[-3000:] + out.stderr[-3000:]
     assert "NO ERROR" not in out.stdout
+
+
+def test_hierarchical_ranks_same_gpu():
+    """K = 2 nodes x L = 2 devices as four ranks on cuda:0 (gloo groups), t2 = 2
+    inner rounds: the per-inner-round node fold and the outer node sum across
+    processes equal the in-process two-level engine bit for bit."""
+    out = _torchrun("--same-gpu", "--nodes", "2", "--devices", "2", "--t2", "2",
+                    script="mp_hier_check.py", nproc=4)
+    assert out.returncode == 0, _why(out)
+    assert "HIER OK" in out.stdout, out.stdout[-2000:]
+
+
+def test_hierarchical_ranks_multi_gpu():
+    n = torch.cuda.device_count()
+    if n < 4:
+        pytest.skip("needs 4 GPUs")
+    out = _torchrun("--nodes", "2", "--devices", "2", "--t2", "3", script="mp_hier_check.py",
+                    nproc=4)
+    assert out.returncode == 0, _why(out)
+    assert "HIER OK" in out.stdout, out.stdout[-2000:]

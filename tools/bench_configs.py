@@ -121,6 +121,123 @@ def c2_modes(args):
     print(json.dumps(res), flush=True)
 
 
+# -------------------------------------------------------- CPU baselines
+def cpu_baselines(om, kind, lam, *, target=None, y=None, rounds_all=3, target_rel=1e-3,
+                  max_epochs=60):
+    """The oracle port (C restatement of the reference, oracle/) on the same
+    arrays: all host cores (CoCoA over nproc host workers, the reference's
+    multi-process mode) for a few rounds, and ONE core (K = 1, the reference's
+    damped_solve with threads_per_device=1) run to the duality-gap target
+    (BASELINE.md §3)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ra = oracle.train(om, kind, lam, target=target, y=y, nodes=cores, epochs=1, seed=0,
+                      rounds=rounds_all, parallel=True, record_obj=False)
+    per_all = float(np.mean(ra["round_s"]))
+    t_all = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r1 = oracle.train(om, kind, lam, target=target, y=y, nodes=1, epochs=1, seed=0,
+                      rounds=max_epochs, target_rel_gap=target_rel)
+    t_one = time.perf_counter() - t0
+    hit = r1["rounds"] if r1["gap"][-1] <= target_rel * abs(r1["objective"][-1]) else None
+    return {"all_cores": {"cores": cores, "epochs_per_s": 1.0 / per_all, "rounds": rounds_all,
+                          "wall_s": t_all, "kind": "port"},
+            "one_core": {"cores": 1, "epochs_per_s": r1["rounds"] / max(sum(r1["round_s"]), 1e-9),
+                         "time_to_target_s": t_one if hit else None, "epochs_to_target": hit,
+                         "target": f"gap <= {target_rel} |F|", "kind": "port",
+                         "includes_gap_checks": True}}
+
+
+def engine_modes(dm, spec, args, alg_bytes, n_coords, seq_rounds=None):
+    """Async (bench's configuration: one attempt per round, fused turn, L1-cached
+    view gathers) and sequential engines: epoch ms, roofline fraction, rounds
+    and device time to gap <= 1e-3 |F|."""
+    out = {}
+    for mode in ("async", "sequential"):
+        rounds = args.rounds if mode == "async" else (seq_rounds or args.seq_rounds)
+        kw = dict(sync_solves=False, retry_budget=0, cache_flags=1) if mode == "async" else {}
+        eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode=mode, **kw)
+        r = timed_rounds(eng, rounds)
+        ms = float(np.median(r["round_ms"][1:] if len(r["round_ms"]) > 2 else r["round_ms"]))
+        out[mode] = {"epoch_ms_median": ms, "epochs_per_s": 1000.0 / ms,
+                     "coord_updates_per_s": n_coords * 1000.0 / ms,
+                     "algorithmic_GBps": alg_bytes / (ms * 1e-3) / 1e9,
+                     "hbm_frac_of_round": alg_bytes / (ms * 1e-3) / 1e9 / HBM,
+                     "rel_gap": r["rel_gap"], "to_1e-3": r["to_target"]}
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+    out["algorithmic_bytes_per_epoch"] = alg_bytes
+    return out
+
+
+# ------------------------------------------------------------ C2 primal
+def c2p(args):
+    """BASELINE configs[1] literally: L2 logistic regression in the PRIMAL
+    (restated kind logistic_primal): coordinates = the 100k features (about
+    400 nnz per column, the long-column path), v = A w over the 1M examples
+    (8 MB), the same synthetic examples as bench.py (labels unfolded)."""
+    import bench
+    import oracle
+    indptr, rows, vals, y = bench.gen_columns(0, bench.N_EX // bench.BLOCK)
+    raw = vals * np.repeat(y, bench.NNZ)             # undo bench's label fold
+    ex = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, raw)
+    dm = ex.transpose()                               # columns = features
+    del ex
+    spec = g.ObjectiveSpec("logistic_primal", bench.LAM, bench.N_EX, bench.D_FEAT, target=y)
+    nnz = bench.N_EX * bench.NNZ
+    res = {"config": "C2-primal", "workload": "L2 logistic regression, PRIMAL SCD "
+           "(logistic_primal), synthetic sparse 1M examples x 100k features, 40 nnz/example "
+           "(~400 per feature column), lambda=1", "nnz": nnz}
+    res.update(engine_modes(dm, spec, args, 12 * nnz + 36 * bench.D_FEAT, bench.D_FEAT))
+    if not args.no_cpu:
+        h = dm.to_host()
+        om = oracle.OMatrix(h.n_rows, h.indptr, h.rows, h.vals)
+        res["cpu_baseline"] = cpu_baselines(om, "logistic_primal", bench.LAM, target=y)
+    print(json.dumps(res), flush=True)
+
+
+# --------------------------------------------------------------- C1 dual
+def c1d(args):
+    """BASELINE configs[0] literally: ridge regression in the DUAL (restated
+    kind dual_ridge): coordinates = the 20k examples (dense columns of 500),
+    v = X^T alpha (500 doubles)."""
+    import oracle
+    n_ex, n_feat = 20_000, 500
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    X = torch.randn(n_ex, n_feat, device="cuda", dtype=torch.float64, generator=gen) / \
+        np.sqrt(n_feat)
+    wt = torch.randn(n_feat, device="cuda", dtype=torch.float64, generator=gen)
+    b = X @ wt + 0.1 * torch.randn(n_ex, device="cuda", dtype=torch.float64, generator=gen)
+    dm = DeviceMatrix(n_feat, n_ex, L.DENSE, X.contiguous().reshape(-1))   # column = example
+    yb = b.cpu().numpy()
+    spec = g.ObjectiveSpec("dual_ridge", 1.0, n_ex, n_feat, target=yb)
+    nnz = n_ex * n_feat
+    res = {"config": "C1-dual", "workload": "ridge regression, DUAL SCD (dual_ridge), dense "
+           "20k x 500, lambda=1", "nnz": nnz}
+    res.update(engine_modes(dm, spec, args, 8 * nnz + 28 * n_ex, n_ex, seq_rounds=args.rounds))
+    if not args.no_cpu:
+        Xh = X.cpu().numpy()
+        indptr = np.arange(0, nnz + 1, n_feat, dtype=np.int64)
+        rws = np.tile(np.arange(n_feat, dtype=np.int32), n_ex)
+        om = oracle.OMatrix(n_feat, indptr, rws, Xh.reshape(-1))
+        res["cpu_baseline"] = cpu_baselines(om, "dual_ridge", 1.0, y=yb)
+    print(json.dumps(res), flush=True)
+
+
+def c2cpu(args):
+    """The bench workload's CPU baselines: the oracle port on
+    all host cores and on one core run to the 1e-3 duality-gap target."""
+    import bench
+    import oracle
+    indptr, rows, vals, _ = bench.gen_columns(0, bench.N_EX // bench.BLOCK)
+    om = oracle.OMatrix(bench.D_FEAT, indptr, rows, vals)
+    res = {"config": "C2-cpu", "workload": "bench.py C2 (dual L2 logistic 1M x 100k, 40 nnz)",
+           "cpu_baseline": cpu_baselines(om, "dual_l2_logistic", bench.LAM)}
+    print(json.dumps(res), flush=True)
+
+
 # ------------------------------------------------------------------ C1
 def c1(args):
     """ridge_primal, dense 20k examples x 500 features (coordinates = features)."""
@@ -276,7 +393,8 @@ def c5(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=("c1", "c2", "c3", "c4", "c5"))
+    ap.add_argument("config", choices=("c1", "c1d", "c2", "c2p", "c2cpu", "c3", "c4", "c5"))
+    ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--lam", type=float, default=None)
     ap.add_argument("--rounds", type=int, default=10)
@@ -296,6 +414,12 @@ def main():
         c3(args)
     elif args.config == "c1":
         c1(args)
+    elif args.config == "c1d":
+        c1d(args)
+    elif args.config == "c2p":
+        c2p(args)
+    elif args.config == "c2cpu":
+        c2cpu(args)
     elif args.config == "c2":
         c2_modes(args)
     elif args.config == "c4":
