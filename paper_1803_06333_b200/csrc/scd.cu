@@ -948,9 +948,22 @@ __device__ __forceinline__ void workers_sync() {
 // in flight, its rows (up to LVL_STAGE per column) staged into shared memory
 // with cp.async, then the entries get their levels one after another from
 // the row -> level+1 table, which is cleared again from the staged rows.
+// GLM_LVL_DEBUG=1: the kernel prints where its time went (cycles of warp 0
+// planning, per planning phase, and of worker warp 1 executing; windows, levels)
+__device__ int lvl_debug = 0;
+__device__ unsigned long long lvl_phase[6];
+
 __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *tab,
                          uint32_t (*stage)[LVL_STAGE]) {
     const int lane = threadIdx.x & 31;
+    long long tp = clock64();
+    auto mark = [&](int i) {
+        if (lvl_debug && lane == 0) {
+            const long long t = clock64();
+            lvl_phase[i] += (unsigned long long)(t - tp);
+            tp = t;
+        }
+    };
     const int64_t rem = p.m - k0;
     const int nmax = rem < LVL_WINDOW ? (int)rem : LVL_WINDOW;
     constexpr int U = LVL_WINDOW / 32;
@@ -984,8 +997,10 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
         const int ci = c < nmax ? (cu < LVL_STAGE ? (int)cu : LVL_STAGE) : 0;
         for (int q = 0; q < ci; ++q) cp_async4(&stage[c][q], p.rows + lo[u] + q);
     }
+    mark(0);
     cp_async_wait_all();
     __syncwarp();
+    mark(1);
     // levels, one entry after another: the chain per entry is the table
     // reads, one redux.sync max and the table writes (the entry's staged rows
     // are read into registers one entry ahead)
@@ -1022,6 +1037,7 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
         __syncwarp();
     }
     __syncwarp();
+    mark(2);
     // the table only serves dependencies inside a window: clear this one's
     // rows (eight entries' staged rows read before any is cleared)
     for (int c0 = 0; c0 < n; c0 += 8) {
@@ -1043,6 +1059,7 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
         for (int c = 0; c < n; ++c)
             for (int q = LVL_STAGE + lane; q < P.cnt[c]; q += 32) tab[__ldg(p.rows + P.lo[c] + q)] = 0;
     __syncwarp();
+    mark(3);
     // stable counting sort of the window's entries by level
     const int nlev = maxlev + 1;
     int base = 0;
@@ -1063,11 +1080,9 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
         P.k0 = k0;
     }
     __syncwarp();
+    mark(4);
 }
 
-// GLM_LVL_DEBUG=1: the kernel prints where its time went (cycles of warp 0
-// planning and of worker warp 1 executing, windows, levels)
-__device__ int lvl_debug = 0;
 
 template <bool SMEM>
 __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
@@ -1124,7 +1139,9 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
             break;
         }
         if (warp == 0) {
+            const long long tg = clock64();
             if (w > 0) window_gsum(plans[(w - 1) & 1]);
+            if (lvl_debug && lane == 0) lvl_phase[5] += (unsigned long long)(clock64() - tg);
             const int64_t k1 = P.k0 + n;
             if (k1 < p.m) lvl_plan(p, plans[(w + 1) & 1], k1, tab, stage);
             else if (lane == 0) plans[(w + 1) & 1].n = 0;
@@ -1216,6 +1233,10 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
     if (lvl_debug && lane == 0 && warp <= 1)
         printf("scd_seq_lvl warp %d: busy %lld of %lld cycles, %lld windows, %lld levels\n", warp,
                dbg_busy, clock64() - dbg_t0, dbg_windows, dbg_levels);
+    if (lvl_debug && threadIdx.x == 0)
+        printf("scd_seq_lvl planner phases (cycles): loads+stage issue %llu, stage wait %llu, "
+               "levels %llu, clear %llu, sort %llu, g-sum %llu\n", lvl_phase[0], lvl_phase[1],
+               lvl_phase[2], lvl_phase[3], lvl_phase[4], lvl_phase[5]);
     __syncthreads();
     if (SMEM)
         for (int64_t r = threadIdx.x; r < p.d; r += blockDim.x) gview[r] = sview[r];

@@ -58,10 +58,12 @@ def main():
         ref = g.train(m, spec, cfg, g.StoppingCriteria(max_rounds=4), mode="sequential")
         o, o_ref = res.trace.objectives(), ref.trace.objectives()
         if kind == "dual_l2_svm":
-            # alpha0 = 0, v0 = 0 exactly: the same additions in the same order
-            assert np.array_equal(o, o_ref), (kind, o, o_ref)
+            # alpha0 = 0, v0 = 0 exactly: alpha and v see the same additions in
+            # the same order (the reported objective sums g over the ranks'
+            # partial sums, so it agrees to rounding only)
             assert np.array_equal(res.v, ref.v)
             assert np.array_equal(res.model.alpha, ref.model.alpha)
+            assert np.allclose(o, o_ref, rtol=1e-13, atol=0), (kind, o, o_ref)
         else:
             # v0 = A alpha0 is summed per rank, then across ranks (one SpMV
             # in-process): rounding-level differences only
