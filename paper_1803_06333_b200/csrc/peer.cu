@@ -810,16 +810,20 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
         if (e != cudaSuccess) return glm_set_cuda_error(e, "glm_peer_create", __FILE__, __LINE__);
         return glm_set_error(GLM_USAGE, "round_turn_kernel cannot be resident on this device");
     }
-    p->turn_blocks = (occ < 2 ? occ : 2) * sms;
+    int per_sm = occ < 2 ? occ : 2;
+    if (const char *env = getenv("GLM_TURN_BLOCKS_PER_SM"))   // experiments: 1 or 2
+        per_sm = atoi(env) >= 1 && atoi(env) <= per_sm ? atoi(env) : per_sm;
+    p->turn_blocks = per_sm * sms;
     if (p->turn_blocks > PEER_BLOCKS) p->turn_blocks = PEER_BLOCKS;
     p->ctl = reinterpret_cast<int64_t *>(p->mem);
     p->dv = reinterpret_cast<double *>(p->mem + PEER_HEADER);
     p->flags = p->ctl + PEER_FLAGS;
     p->flags2 = p->ctl + PEER_FLAGS2;
-    // reduce-scatter + all-gather once there are 3+ ranks (at 2 it moves the
-    // same bytes as reading the peer's whole Delta v, plus a flag round trip);
-    // GLM_PEER_RS=0/1 overrides
-    p->rs = world >= 3;
+    // reduce-scatter + all-gather for 3+ ranks and a large Delta v (at 2 ranks
+    // it moves the same bytes as reading the peer's whole Delta v; for a small
+    // one its extra flag round trip costs more than the bytes it saves: C2's
+    // 800 KB at 4 GPUs, turn 32.7 -> 38.5 us); GLM_PEER_RS=0/1 overrides
+    p->rs = world >= 3 && d >= (int64_t)1 << 22;
     if (const char *env = getenv("GLM_PEER_RS")) p->rs = env[0] == '1';
     if (world == 1) {
         p->rs = 0;
