@@ -491,6 +491,10 @@ def ours_main(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_arm(args, budget_s=args.cpu_budget)
+    primal = None
+    if world == 1 and not args.no_primal:
+        primal = primal_leg(args, g, indptr, rows, vals, y)
+        phase("primal leg done", rank)
 
     if rank == 0:
         roofline["l2_random_ceiling"] = l2_ceiling(nnz_loc, epoch_ms)
@@ -502,6 +506,7 @@ def ours_main(args):
                 "coord_updates_per_s": value * N_EX,
                 "time_to_target": ttt, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+                "c2_primal": primal,
                 "solver_state": {"retries_last_round": int(res_state.retries),
                                  "epochs_run_last_round": int(res_state.epochs_run),
                                  "damping": float(res_state.damping)}}
@@ -572,6 +577,57 @@ def ttt_graph(eng, rounds, world):
             "final_objective": float(best[3]),
             "timer": "device: CUDA events inside one graph replay (rounds + fused gap kernels "
                      "after every round), best of 2 replays after a warm one, max over ranks"}
+
+
+def primal_leg(args, g, indptr, rows, vals, y):
+    """BASELINE configs[1] as worded: the same examples trained in the PRIMAL
+    (restated kind logistic_primal: coordinates = the 100k features, ~400 nnz
+    per column; v = X w over the 1M examples).  Same engine configuration as
+    the headline (async, one attempt per round, fused turn, graph replay)."""
+    import torch
+    from paper_1803_06333_b200.data import DeviceMatrix
+    raw = vals * np.repeat(y, NNZ)                    # undo the label fold
+    ex = DeviceMatrix.from_csc(D_FEAT, indptr, rows, raw)
+    dm = ex.transpose()                                # columns = features
+    del ex
+    spec = g.ObjectiveSpec("logistic_primal", LAM, N_EX, D_FEAT, target=y)
+    eng = g.Engine(dm, spec, g.HierarchyConfig(nodes=1, devices=1, t1=10 ** 6, seed=0, epochs=1),
+                   mode="async", sync_solves=False, retry_budget=0, cache_flags=args.cache_flags)
+    obj, gap = eng.objective_and_gap()
+    rounds = 0
+    while gap > 1e-3 * abs(obj) and rounds < 50:
+        eng.outer_round()
+        rounds += 1
+        obj, gap = eng.objective_and_gap()
+    traj = 10
+    eng.reset()
+    graph = eng.capture(traj)
+    times = []
+    for _ in range(4):
+        eng.reset()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        graph.replay()
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = float(np.median(times[1:])) / traj
+    del graph
+    ttt = ttt_graph(eng, rounds, 1)
+    eng.close()
+    nnz = N_EX * NNZ
+    alg = 12 * nnz + 36 * D_FEAT
+    peak, _ = measured_peaks()
+    return {"workload": "C2 as BASELINE configs[1] words it: L2 logistic regression, PRIMAL SCD "
+                        "(restated kind logistic_primal), 100k feature coordinates (~400 nnz "
+                        "each), v over the 1M examples, the headline's examples and labels",
+            "epochs_per_s": 1000.0 / ms, "ms_per_step": ms,
+            "hbm_frac_of_step": alg / (ms * 1e-3) / 1e9 / peak,
+            "algorithmic_bytes_per_epoch": alg,
+            "time_to_target": dict(ttt, epochs_host_loop=rounds,
+                                   target="duality gap <= 1e-3 * |F|"),
+            "timed": "10-epoch trajectories from alpha0 replayed as one CUDA graph, median of 3"}
 
 
 def e2e_leg(args, g, device_solve_host, indptr, rows, vals, spec, reducer, world):
@@ -655,6 +711,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-primal", action="store_true",
+                    help="skip the C2-primal leg (BASELINE configs[1] as worded)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--graph", type=int, default=1, help="replay trajectories as CUDA graphs")
     ap.add_argument("--traj", type=int, default=20,
