@@ -28,7 +28,7 @@ def _ragged(n, d, seed, max_nnz=60, long_every=0):
     """Columns of 0..max_nnz distinct rows (some empty); every `long_every`-th
     column has 150 rows (the > 96-entry tail path)."""
     rng = np.random.default_rng(seed)
-    counts = rng.integers(0, max_nnz + 1, size=n)
+    counts = rng.integers(0, min(max_nnz, d) + 1, size=n)
     if long_every:
         counts[::long_every] = 150
     indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
@@ -66,15 +66,19 @@ def _solve(m, kind, lam, epochs, seed, env):
     (60_000, 40_000, 37, "dual_l2_logistic"),    # view in L2, tail columns
     (50_000, 100_000, 0, "dual_l2_svm"),         # C2's d
     (3_000, 200, 0, "dual_l2_svm"),              # dense conflicts: many levels per window
+    (1_000, 40, 0, "dual_l2_logistic"),          # up to 40 of 40 rows: > 15 levels per window
 ])
 def test_level_kernel_bit_identical_to_one_warp_walk(n, d, long_every, kind):
+    """The level-scheduled kernel (default) and GLM_SEQ_KERNEL=csc (the
+    one-warp walk): identical bits."""
     m = _ragged(n, d, seed=n + d, long_every=long_every)
-    lv, s_lv, _ = _solve(m, kind, 1.0, 3, 5, None)
     cs, s_cs, _ = _solve(m, kind, 1.0, 3, 5, "csc")
-    assert s_lv == s_cs and lv.epochs_run == cs.epochs_run and lv.retries == cs.retries
-    assert np.asarray(lv.delta_alpha).tobytes() == np.asarray(cs.delta_alpha).tobytes()
-    assert np.asarray(lv.delta_v).tobytes() == np.asarray(cs.delta_v).tobytes()
-    assert list(lv.epoch_values) == list(cs.epoch_values)
+    for env in (None,):
+        lv, s_lv, _ = _solve(m, kind, 1.0, 3, 5, env)
+        assert s_lv == s_cs and lv.epochs_run == cs.epochs_run and lv.retries == cs.retries
+        assert np.asarray(lv.delta_alpha).tobytes() == np.asarray(cs.delta_alpha).tobytes(), env
+        assert np.asarray(lv.delta_v).tobytes() == np.asarray(cs.delta_v).tobytes(), env
+        assert list(lv.epoch_values) == list(cs.epoch_values), env
 
 
 def test_full_c2_deterministic_epoch_vs_reference_oracle():
