@@ -1060,8 +1060,20 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
             for (int q = LVL_STAGE + lane; q < P.cnt[c]; q += 32) tab[__ldg(p.rows + P.lo[c] + q)] = 0;
     __syncwarp();
     mark(3);
-    // stable counting sort of the window's entries by level
-    const int nlev = maxlev + 1;
+    if (lane == 0) {
+        P.n = n;
+        P.nlev = maxlev + 1;
+        P.k0 = k0;
+    }
+    __syncwarp();
+    mark(4);
+}
+
+// One executing warp: the stable counting sort of the planned window's
+// entries by level (order, lstart) — off the planner's critical path.
+__device__ void lvl_sort(LvlPlan &P) {
+    const int lane = threadIdx.x & 31;
+    const int n = P.n, nlev = P.nlev;
     int base = 0;
     for (int L = 0; L < nlev; ++L) {
         if (lane == 0) P.lstart[L] = (uint16_t)base;
@@ -1073,14 +1085,8 @@ __device__ void lvl_plan(const EpochParams &p, LvlPlan &P, int64_t k0, uint8_t *
             base += __popc(bal);
         }
     }
-    if (lane == 0) {
-        P.lstart[nlev] = (uint16_t)base;
-        P.n = n;
-        P.nlev = nlev;
-        P.k0 = k0;
-    }
+    if (lane == 0) P.lstart[nlev] = (uint16_t)base;
     __syncwarp();
-    mark(4);
 }
 
 
@@ -1123,30 +1129,16 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
         LvlPlan &P = plans[w & 1];
         const int n = P.n;
         const long long dbg_w0 = clock64();
-        // the previous window's g terms: g(b + delta) evaluated lane-parallel
-        // off the workers' critical path, then summed in permutation order
-        // (scd_seq_csc's sum, the same bits)
-        auto window_gsum = [&](LvlPlan &Q) {
-            for (int c = lane; c < Q.n; c += 32)
-                Q.gterm[c] = g_one(kind, p.lam, p.rho, Q.gy[c], Q.gterm[c]);
-            __syncwarp();
-            if (lane == 0)
-                for (int c = 0; c < Q.n; ++c) gacc += Q.gterm[c];
-            __syncwarp();
-        };
-        if (n == 0) {
-            if (warp == 0 && w > 0) window_gsum(plans[(w - 1) & 1]);     // the last window
-            break;
-        }
+        if (n == 0) break;
         if (warp == 0) {
-            const long long tg = clock64();
-            if (w > 0) window_gsum(plans[(w - 1) & 1]);
-            if (lvl_debug && lane == 0) lvl_phase[5] += (unsigned long long)(clock64() - tg);
             const int64_t k1 = P.k0 + n;
             if (k1 < p.m) lvl_plan(p, plans[(w + 1) & 1], k1, tab, stage);
             else if (lane == 0) plans[(w + 1) & 1].n = 0;
         } else {
             const int me = warp - 1;
+            const int tw = me * 32 + lane;
+            if (me == 0) lvl_sort(P);           // order / lstart of this window
+            workers_sync();
             auto load = [&](int e, Col &c) {
                 const int slot = P.order[e];
                 c.slot = slot;
@@ -1225,6 +1217,16 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
                 ++cur_level;
             }
             dbg_levels += nlev;
+            // g(b + delta) of the window's entries in parallel, then summed in
+            // permutation order (scd_seq_csc's sum: the same bits)
+            const long long tg = clock64();
+            for (int c = tw; c < n; c += LVL_WORKERS * 32)
+                P.gterm[c] = g_one(kind, p.lam, p.rho, P.gy[c], P.gterm[c]);
+            workers_sync();
+            if (tw == 0) {
+                for (int c = 0; c < n; ++c) gacc += P.gterm[c];
+                if (lvl_debug) lvl_phase[5] += (unsigned long long)(clock64() - tg);
+            }
         }
         dbg_busy += clock64() - dbg_w0;
         ++dbg_windows;
@@ -1235,12 +1237,12 @@ __global__ void __launch_bounds__(LVL_THREADS) scd_seq_lvl(EpochParams p) {
                dbg_busy, clock64() - dbg_t0, dbg_windows, dbg_levels);
     if (lvl_debug && threadIdx.x == 0)
         printf("scd_seq_lvl planner phases (cycles): loads+stage issue %llu, stage wait %llu, "
-               "levels %llu, clear %llu, sort %llu, g-sum %llu\n", lvl_phase[0], lvl_phase[1],
+               "levels %llu, clear %llu, bookkeeping %llu; workers' g-sum %llu\n", lvl_phase[0], lvl_phase[1],
                lvl_phase[2], lvl_phase[3], lvl_phase[4], lvl_phase[5]);
     __syncthreads();
     if (SMEM)
         for (int64_t r = threadIdx.x; r < p.d; r += blockDim.x) gview[r] = sview[r];
-    if (threadIdx.x == 0) {
+    if (warp == 1 && lane == 0) {      // the workers' first thread holds the g-sum
         p.gpart[0] = gacc;
         st->epoch_blocks = 1;
     }
