@@ -344,8 +344,14 @@ int glm_stream_create_file(int device, const char *path, int64_t n_rows, int n_c
                            const int64_t *chunk_offsets, const int64_t *chunk_cols,
                            const int64_t *chunk_nnz, int64_t device_budget, glm_stream **out);
 int glm_stream_destroy(glm_stream *s);
-/* out[7] = n_chunks, resident chunks, resident bytes, streaming-slot bytes,
- * direct DMA (0/1), n_cols, n_rows */
+/* File streams only: read streamed chunk bodies with O_DIRECT (the page cache
+ * bypassed: an aligned superset of each body into the pinned staging buffer;
+ * falls back to buffered reads where the file system refuses O_DIRECT — see
+ * glm_stream_info out[7]) and with io_threads concurrent preads per body.
+ * Buffered reads also advise the kernel to read the next chunk ahead. */
+int glm_stream_set_io(glm_stream *s, int direct_io, int io_threads);
+/* out[8] = n_chunks, resident chunks, resident bytes, streaming-slot bytes,
+ * direct DMA (0/1), n_cols, n_rows, O_DIRECT reads active (0/1) */
 int glm_stream_info(const glm_stream *s, int64_t *out);
 /* `epochs` passes over every chunk (chunked_device_runner's runner body).
  * delta_io f64[n_cols] (in with GLM_STREAM_DELTA_IN; out: the partition's

@@ -120,6 +120,7 @@ SIGNATURES = {
                                               _P, _P, _P, _c_i64, _P]),
     "glm_stream_destroy": (ctypes.c_int, [_P]),
     "glm_stream_info": (ctypes.c_int, [_P, _P]),
+    "glm_stream_set_io": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
     "glm_stream_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "glm_stream_schedule": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
     "glm_peer_create": (ctypes.c_int, [ctypes.c_int, _c_i64, ctypes.c_int, ctypes.c_int, _P]),

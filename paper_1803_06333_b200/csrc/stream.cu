@@ -79,6 +79,9 @@ struct glm_stream {
     bool direct = false;               // host arrays are pinned: DMA straight from them
     std::vector<void *> registered;    // cudaHostRegister'ed ranges (unregistered on destroy)
     int fd = -1;
+    int dfd = -1;                      // O_DIRECT descriptor (glm_stream_set_io), -1 = buffered
+    int io_threads = 1;                // concurrent pread stripes per chunk body
+    std::string path;
     std::vector<int64_t> foff;         // file offset of chunk c's indptr
     // device
     std::vector<glm::DevChunk> res;    // resident chunks [0, n_res)
@@ -155,6 +158,50 @@ bool pread_all(int fd, void *dst, int64_t bytes, int64_t off) {
     return true;
 }
 
+// [off, off + len) into dst with `threads` concurrent preads (NVMe wants
+// queue depth).  With O_DIRECT the stripes are 4 KiB-aligned and the range
+// may run past EOF: `need` bytes must arrive, the rest may come up short.
+bool pread_striped(int fd, char *dst, int64_t len, int64_t off, int threads, bool direct,
+                   int64_t need) {
+    if (threads <= 1 || len < (4 << 20)) {
+        if (!direct) return pread_all(fd, dst, len, off);
+        int64_t got = 0;
+        while (got < len) {
+            const ssize_t r = pread(fd, dst + got, (size_t)(len - got), (off_t)(off + got));
+            if (r <= 0) break;
+            got += r;
+        }
+        return got >= need;
+    }
+    int64_t stripe = (len + threads - 1) / threads;
+    stripe = (stripe + 4095) & ~(int64_t)4095;
+    std::vector<std::thread> th;
+    std::vector<int64_t> got(threads, 0);
+    auto work = [&](int t) {
+        const int64_t a = (int64_t)t * stripe, b = std::min(len, a + stripe);
+        int64_t k = 0;
+        while (a + k < b) {
+            const ssize_t r = pread(fd, dst + a + k, (size_t)(b - a - k), (off_t)(off + a + k));
+            if (r <= 0) break;
+            k += r;
+        }
+        got[t] = k;
+    };
+    for (int t = 1; t < threads; ++t)
+        if ((int64_t)t * stripe < len) th.emplace_back(work, t);
+    work(0);
+    for (auto &x : th) x.join();
+    int64_t covered = 0;                       // contiguous bytes from the start
+    for (int t = 0; t < threads; ++t) {
+        const int64_t a = (int64_t)t * stripe;
+        if (a >= len) break;
+        const int64_t want = std::min(len, a + stripe) - a;
+        covered = a + got[t];
+        if (got[t] < want) break;
+    }
+    return covered >= need;
+}
+
 // Copy chunk c into device home `h` on stream `xs` (staging through pinned
 // buffer `stage_i` unless the host source is pinned).  Records h.loaded.
 int load_chunk(glm_stream *S, int c, DevChunk &h, int stage_i, double *load_ms) {
@@ -200,8 +247,22 @@ int load_chunk(glm_stream *S, int c, DevChunk &h, int stage_i, double *load_ms) 
         GLM_CUDA_TRY(cudaEventSynchronize(S->stage_free[stage_i]));
         char *st = S->stage[stage_i];
         const int64_t body = 8 * (nc + 1) + 12 * nz;
-        if (!pread_all(S->fd, st, body, S->foff[c]))
-            return glm_set_error(GLM_USAGE, "chunk store read failed (truncated file?)");
+        const int64_t off = S->foff[c];
+        if (S->dfd >= 0) {             // O_DIRECT: the aligned superset, the body at an offset
+            const int64_t a0 = off & ~(int64_t)4095;
+            const int64_t a1 = (off + body + 4095) & ~(int64_t)4095;
+            if (!pread_striped(S->dfd, st, a1 - a0, a0, S->io_threads, true, off + body - a0))
+                return glm_set_error(GLM_USAGE, "chunk store read failed (truncated file?)");
+            st += off - a0;
+        } else {
+            if (!pread_striped(S->fd, st, body, off, S->io_threads, false, body))
+                return glm_set_error(GLM_USAGE, "chunk store read failed (truncated file?)");
+            if (c + 1 < S->n_chunks) {  // read-ahead of the next chunk's body
+                const int64_t nc1 = S->col_off[c + 2] - S->col_off[c + 1];
+                posix_fadvise(S->fd, (off_t)S->foff[c + 1], (off_t)(8 * (nc1 + 1) + 12 * S->nnz[c + 1]),
+                              POSIX_FADV_WILLNEED);
+            }
+        }
         *load_ms = now_ms() - t0;
         GLM_CUDA_TRY(cudaEventRecord(h.copy0, S->xs));
             GLM_CUDA_TRY(cudaMemcpyAsync(h.indptr, st, 8 * (nc + 1), cudaMemcpyHostToDevice, S->xs));
@@ -321,9 +382,11 @@ int setup_device(glm_stream *S, int64_t budget) {
         GLM_CUDA_TRY(cudaEventCreateWithFlags(&S->stage_free[i], cudaEventDisableTiming));
     }
     if (!S->direct || S->src == 1) {
-        S->stage_cap = max_bytes;
+        // + 8 KiB: an O_DIRECT read covers the body's aligned superset
+        S->stage_cap = max_bytes + (S->src == 1 ? 8192 : 0);
         for (int i = 0; i < 2; ++i)
-            GLM_CUDA_TRY(cudaHostAlloc((void **)&S->stage[i], (size_t)max_bytes, cudaHostAllocDefault));
+            GLM_CUDA_TRY(cudaHostAlloc((void **)&S->stage[i], (size_t)S->stage_cap,
+                                       cudaHostAllocDefault));
     }
     int rc = glm_solver_create(S->device, max_cols, S->d, &S->solver);
     if (rc) return rc;
@@ -382,6 +445,7 @@ int glm_stream_destroy(glm_stream *S) {
     if (S->cs) cudaStreamDestroy(S->cs);
     if (S->xs) cudaStreamDestroy(S->xs);
     if (S->fd >= 0) close(S->fd);
+    if (S->dfd >= 0) close(S->dfd);
     cudaSetDevice(prev);
     delete S;
     return GLM_OK;
@@ -470,6 +534,7 @@ int glm_stream_create_file(int device, const char *path, int64_t n_rows, int n_c
         S->foff.push_back(chunk_offsets[c] + 12);   // skip the <IQ chunk head (data.py:341)
     }
     S->m = S->col_off.back();
+    S->path = path;
     S->fd = open(path, O_RDONLY);
     if (S->fd < 0) {
         glm_stream_destroy(S);
@@ -484,6 +549,20 @@ int glm_stream_create_file(int device, const char *path, int64_t n_rows, int n_c
     return GLM_OK;
 }
 
+int glm_stream_set_io(glm_stream *S, int direct_io, int io_threads) {
+    if (!S) return glm_set_error(GLM_USAGE, "null stream");
+    if (S->src != 1) return glm_set_error(GLM_USAGE, "I/O options apply to GLMCHUNK file streams");
+    S->io_threads = io_threads < 1 ? 1 : (io_threads > 32 ? 32 : io_threads);
+    if (S->dfd >= 0) {
+        close(S->dfd);
+        S->dfd = -1;
+    }
+    // the file system may not support O_DIRECT (tmpfs): buffered reads then,
+    // reported by glm_stream_info out[7]
+    if (direct_io) S->dfd = open(S->path.c_str(), O_RDONLY | O_DIRECT);
+    return GLM_OK;
+}
+
 int glm_stream_info(const glm_stream *S, int64_t *out) {
     if (!S || !out) return glm_set_error(GLM_USAGE, "null argument");
     out[0] = S->n_chunks;
@@ -493,6 +572,7 @@ int glm_stream_info(const glm_stream *S, int64_t *out) {
     out[4] = S->direct ? 1 : 0;
     out[5] = S->m;
     out[6] = S->d;
+    out[7] = S->dfd >= 0 ? 1 : 0;
     return GLM_OK;
 }
 

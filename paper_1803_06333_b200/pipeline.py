@@ -180,7 +180,7 @@ class StreamingPartition:
     (None: everything that fits, i.e. no streaming after the first epoch)."""
 
     def __init__(self, source, chunk_size=None, chunk_offsets=None, device_budget=None,
-                 pin_host=False, device=None):
+                 pin_host=False, device=None, direct_io=False, io_threads=1):
         _D().require_cuda()
         self.device = torch.cuda.current_device() if device is None else int(device)
         budget = -1 if device_budget is None else int(device_budget)
@@ -197,6 +197,9 @@ class StreamingPartition:
                 self.device, str(source.path).encode(), int(source.n_rows), len(descs),
                 _vp(offs), _vp(cols), _vp(nnz), budget, ctypes.byref(h)), "glm_stream_create_file")
             self.n_rows, self.n_cols = int(source.n_rows), int(self.offsets[-1])
+            if direct_io or io_threads > 1:     # streamed chunks: O_DIRECT / striped preads
+                L.check(L.lib().glm_stream_set_io(h, 1 if direct_io else 0, int(io_threads)),
+                        "glm_stream_set_io")
         else:
             m = source
             n = int(m.n_cols)
@@ -215,8 +218,9 @@ class StreamingPartition:
                 ctypes.byref(h)), "glm_stream_create_host")
             self.n_rows, self.n_cols = int(m.n_rows), n
         self.handle = h
-        info = np.zeros(7, dtype=np.int64)
+        info = np.zeros(8, dtype=np.int64)
         L.check(L.lib().glm_stream_info(h, _vp(info)), "glm_stream_info")
+        self.direct_io = bool(info[7])
         self.n_chunks, self.n_resident = int(info[0]), int(info[1])
         self.bytes_resident, self.bytes_slots = int(info[2]), int(info[3])
         self.direct_dma = bool(info[4])
@@ -239,7 +243,7 @@ class StreamingPartition:
               dv_out=None, coord_target=None, timing=False, group_lanes=0, max_inflight=0,
               attempts_per_chunk=0, cache_flags=0):
         """`epochs` chunked passes (chunked_device_runner's runner body,
-        pipeline.py:315-340). Returns (delta, values, info, scal, damping)."""
+        pipeline.py:315-340). Returns (status, delta, values, info, scal, damping)."""
         from .solver import _KIND_INDEX
         m, d = self.n_cols, self.n_rows
         lin, base = _as_f64(lin), _as_f64(base)

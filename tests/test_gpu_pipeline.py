@@ -87,10 +87,12 @@ def test_streamed_equals_resident_bits_host_and_file(tmp_path):
     g.write_chunks(m, 1_000, tmp_path / "s.chunks")
     store = g.open_chunks(tmp_path / "s.chunks")
     outs = []
-    for src, budget, pin in [("host", None, False), ("host", 1, False), ("host", 1, True),
-                             ("file", 1, False), ("file", 600_000, False)]:
+    for src, budget, pin, dio in [("host", None, False, False), ("host", 1, False, False),
+                                  ("host", 1, True, False), ("file", 1, False, False),
+                                  ("file", 600_000, False, False), ("file", 1, False, True)]:
+        kw = dict(direct_io=True, io_threads=4) if dio else {}
         part = P.StreamingPartition(store if src == "file" else m, chunk_size=1_000,
-                                    device_budget=budget, pin_host=pin)
+                                    device_budget=budget, pin_host=pin, **kw)
         if budget == 600_000:
             assert 0 < part.n_resident < part.n_chunks      # resident prefix + streaming
         runner = P.chunked_device_runner(part, seed=5, epochs=3)
@@ -100,6 +102,31 @@ def test_streamed_equals_resident_bits_host_and_file(tmp_path):
     for obj, alpha in outs[1:]:
         np.testing.assert_array_equal(obj, outs[0][0])
         np.testing.assert_array_equal(alpha, outs[0][1])
+
+
+def test_file_stream_direct_io_and_striped_reads(tmp_path):
+    """Chunk bodies of 12 MB read from a GLMCHUNK file with O_DIRECT (aligned
+    supersets into the pinned staging buffers; buffered where the file system
+    refuses it) and with 4 concurrent stripes: the same bits as the buffered
+    single-thread reader and as the resident run."""
+    m = _synth(400_000, 20_000, 10, 11)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
+    g.write_chunks(m, 100_000, tmp_path / "big.chunks")
+    store = g.open_chunks(tmp_path / "big.chunks")
+    outs = []
+    for budget, kw in [(None, {}), (1, {}), (1, dict(io_threads=4)),
+                       (1, dict(direct_io=True, io_threads=4)), (1, dict(direct_io=True))]:
+        part = P.StreamingPartition(store, device_budget=budget, **kw)
+        if budget == 1:
+            assert part.n_resident == 0
+        runner = P.chunked_device_runner(part, seed=3, epochs=2)
+        res = _train(m, spec, runner, 1, 2, 2)
+        outs.append((res.trace.objectives(), res.model.alpha, part.direct_io))
+        part.close()
+    for obj, alpha, _ in outs[1:]:
+        np.testing.assert_array_equal(obj, outs[0][0])
+        np.testing.assert_array_equal(alpha, outs[0][1])
+    print("O_DIRECT active:", outs[3][2])
 
 
 def test_host_buffers_runner_drop_in():
