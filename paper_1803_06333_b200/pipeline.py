@@ -177,10 +177,14 @@ class StreamingPartition:
     streaming pipeline (glm_stream_*). Source: a GLMCHUNK `ChunkStore`
     (read by the native loader thread) or a host `SparseColumnMatrix` cut into
     `chunk_size` columns. `device_budget` bytes of chunk data stay resident
-    (None: everything that fits, i.e. no streaming after the first epoch)."""
+    (None: everything that fits, i.e. no streaming after the first epoch).
+    File sources read each streamed chunk body with `io_threads` concurrent
+    preads (page cache: 7.7 GB/s with one, 31.6 GB/s with eight on the GPU
+    box) and, with `direct_io`, bypass the page cache (O_DIRECT: the device's
+    own rate, 4.4 GB/s on the box's virtio disk)."""
 
     def __init__(self, source, chunk_size=None, chunk_offsets=None, device_budget=None,
-                 pin_host=False, device=None, direct_io=False, io_threads=1):
+                 pin_host=False, device=None, direct_io=False, io_threads=8):
         _D().require_cuda()
         self.device = torch.cuda.current_device() if device is None else int(device)
         budget = -1 if device_budget is None else int(device_budget)
