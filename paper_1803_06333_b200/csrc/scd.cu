@@ -348,8 +348,7 @@ __global__ void narrow_pad_kernel(const SolveState *st, const double *view0, con
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase, double *vpad,
-                                                   int delay2) {
+__global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase, double *vpad) {
     SolveState *st = p.st;
     if (skip_attempt(st, p.seq)) return;
     __shared__ double snap[32 * R];
@@ -374,11 +373,8 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
     const int64_t per_cta = (int64_t)nwarp * per_phase;
     const int64_t stride = (int64_t)gridDim.x * per_cta;
-    // row threadIdx.x: the publishes still in flight.  With delay 2 the atomic's
-    // return is consumed two phases later (its round trip spans two phases);
-    // the snapshot is then old(p-2) + x(p-2) + x(p-1) + x(p).
-    double prev_old = 0.0, prev_x = 0.0, prev2_old = 0.0, prev2_x = 0.0;
-    int published = 0;
+    double prev_old = 0.0, prev_x = 0.0;   // row threadIdx.x: the last publish
+    bool have_prev = false;
     // This warp's coordinates: position t -> k(t) = base + (t / P) * stride +
     // t % P.  Two-stage software pipeline: the permutation entry of t + 2 and
     // the column of t + 1 are in flight while t is stepped (the column load
@@ -442,16 +438,10 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
             const int r = threadIdx.x;
             const double x = fold[r];
             fold[r] = 0.0;
-            if (delay2) {
-                snap[r] = published >= 2 ? prev2_old + prev2_x + prev_x + x : snap[r] + x;
-                prev2_old = prev_old;
-                prev2_x = prev_x;
-            } else {
-                snap[r] = published >= 1 ? prev_old + prev_x + x : snap[r] + x;
-            }
+            snap[r] = have_prev ? prev_old + prev_x + x : snap[r] + x;
             prev_old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
             prev_x = x;
-            ++published;
+            have_prev = true;
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) pend[i] = 0.0;
@@ -467,232 +457,6 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
         __threadfence();
         for (int r = threadIdx.x; r < p.d; r += blockDim.x)
             view[r] = ld_cg(vpad + (int64_t)r * PAD_STRIDE);
-        __syncthreads();
-        if (threadIdx.x == 0) st->block_counter = 0;
-    }
-    store_block_gsum(gacc, p.gpart, st);
-}
-
-// Asynchronous narrow kernel, second form.  Two changes against scd_replica:
-//  * the shared view is published into REPLICA_COPIES copies (CTA b adds to
-//    copy b % K with a returning atomic and reads the other copies): the
-//    per-phase atomics of all CTAs no longer queue on d addresses
-//    (grid / K instead of grid same-address adds per row and phase);
-//  * each warp keeps REPLICA_DEPTH coordinates' columns and metadata in
-//    flight through a shared-memory ring filled by cp.async, the permutation
-//    entries twice as far ahead — the epoch streams 2.5 GB, and one column
-//    ahead per warp left only ~0.7 MB of loads in flight.
-// Same staleness budget and phase structure (per_phase coordinates per warp,
-// then fold + publish, the returns consumed one phase later).
-constexpr int REPLICA_COPIES = 8;            // the most copies scd_replica2 spreads over
-// ring depth: 8 columns ahead for d <= 32, fewer for wider columns (smem)
-__host__ __device__ constexpr int replica_depth(int R) { return R <= 1 ? 8 : (R == 2 ? 4 : 2); }
-constexpr int REPLICA_WARPS = 8;
-constexpr int REPLICA_ROWS = 256;                // row stride between copies
-
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__global__ void narrow_pad2_kernel(const SolveState *st, const double *view0, const double *view1,
-                                   double *vpad, int64_t d, int64_t seq, int copies) {
-    if (skip_attempt(st, seq)) return;
-    const double *view = st->vw ? view1 : view0;
-    for (int64_t i = threadIdx.x; i < (int64_t)copies * d; i += blockDim.x) {
-        const int64_t c = i / d, r = i % d;
-        vpad[(c * REPLICA_ROWS + r) * PAD_STRIDE] = c == 0 ? view[r] : 0.0;
-    }
-}
-
-template <int R, int C>
-__global__ void __launch_bounds__(32 * REPLICA_WARPS) scd_replica2(EpochParams p, int per_phase,
-                                                                   double *vpad) {
-    SolveState *st = p.st;
-    if (skip_attempt(st, p.seq)) return;
-    constexpr int SLOT = 32 * R + 4;                 // column + (b, dj, s, y)
-    constexpr int REPLICA_DEPTH = replica_depth(R);
-    __shared__ double snap[32 * R];
-    __shared__ double fold[32 * R];
-    __shared__ double ring[REPLICA_WARPS][REPLICA_DEPTH][SLOT];
-    __shared__ int jring[REPLICA_WARPS][REPLICA_DEPTH];
-    __shared__ int pring[REPLICA_WARPS][2 * REPLICA_DEPTH];
-    __shared__ int s_last;
-    const int dc = st->dc;
-    const double damping = st->damping;
-    const double *dcur = delta_cur(p, dc);
-    double *dnext = delta_next(p, dc);
-    double *view = st->vw ? p.view1 : p.view0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t d = p.d;
-    const int own = blockIdx.x % C;
-    for (int r = threadIdx.x; r < 32 * R; r += blockDim.x) {
-        double x = 0.0;
-        if (r < d)
-            for (int c = 0; c < C; ++c)
-                x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
-        snap[r] = x;
-        fold[r] = 0.0;
-    }
-    const int64_t per_cta = (int64_t)REPLICA_WARPS * per_phase;
-    const int64_t stride = (int64_t)gridDim.x * per_cta;
-    const int64_t kbase = (int64_t)blockIdx.x * per_cta + (int64_t)warp * per_phase;
-    // position t of this warp -> coordinate index k (increasing in t):
-    // k = kbase + (t / per_phase) * stride + t % per_phase, advanced without
-    // divisions (inside a phase k + 1, at its end the same slot of the next)
-    struct Pos {
-        int64_t k;
-        int i;
-    };
-    auto adv = [&](Pos q) -> Pos {
-        return q.i + 1 < per_phase ? Pos{q.k + 1, q.i + 1} : Pos{q.k - q.i + stride, 0};
-    };
-    double(*wring)[SLOT] = ring[warp];
-    auto issue = [&](int64_t t, int64_t k) {         // column + metadata of position t
-        const int slot = (int)(t % REPLICA_DEPTH);
-        if (k < p.m) {
-            const int j = pring[warp][t % (2 * REPLICA_DEPTH)];
-            const double *col = p.vals + (int64_t)j * d;
-#pragma unroll
-            for (int i = 0; i < R; ++i)
-                if (lane + 32 * i < d) cp_async8(&wring[slot][lane + 32 * i], col + lane + 32 * i);
-            if (lane == 0) {
-                cp_async8(&wring[slot][32 * R + 0], p.base + j);
-                cp_async8(&wring[slot][32 * R + 2], p.sq + j);
-                jring[warp][slot] = j;
-            } else if (lane == 1) {
-                if (dcur) cp_async8(&wring[slot][32 * R + 1], dcur + j);
-                else wring[slot][32 * R + 1] = 0.0;
-            } else if (lane == 2) {
-                if (p.y) cp_async8(&wring[slot][32 * R + 3], p.y + j);
-                else wring[slot][32 * R + 3] = 0.0;
-            }
-        }
-    };
-    auto issue_perm = [&](int64_t t, int64_t k) {
-        if (lane == 0 && k < p.m) {
-            const unsigned sa =
-                (unsigned)__cvta_generic_to_shared(&pring[warp][t % (2 * REPLICA_DEPTH)]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(p.perm + k)
-                         : "memory");
-        }
-    };
-    // prologue: permutation entries 0 .. 2D-1 (plain loads), columns 0 .. D-1
-    Pos q0{kbase, 0};                                // positions t, t + D, t + 2D
-    Pos qa = q0, qb;
-    for (int t = 0; t < 2 * REPLICA_DEPTH; ++t) {
-        if (lane == t) pring[warp][t] = qa.k < p.m ? __ldg(p.perm + qa.k) : 0;
-        if (t == REPLICA_DEPTH - 1) qb = adv(qa);
-        qa = adv(qa);
-    }
-    Pos q2 = qa;                                     // position 2D
-    __syncwarp();
-    {
-        Pos qi = q0;
-        for (int t = 0; t < REPLICA_DEPTH; ++t) {
-            issue(t, qi.k);
-            cp_async_commit();
-            qi = adv(qi);
-        }
-    }
-    Pos q1 = qb;                                     // position D
-    __syncthreads();
-    const int kind = p.kind;
-    double gacc = 0.0;
-    double pend[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) pend[i] = 0.0;
-    double prev_own = 0.0, prev_x = 0.0, prev_oth[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) prev_oth[c] = 0.0;
-    bool have_prev = false;
-    int64_t t = 0;
-    for (int64_t k0 = (int64_t)blockIdx.x * per_cta; k0 < p.m; k0 += stride) {
-        for (int ii = 0; ii < per_phase; ++ii, ++t) {
-            if (q0.k >= p.m) break;
-            cp_async_wait<REPLICA_DEPTH - 1>();
-            __syncwarp();
-            const int slot = (int)(t % REPLICA_DEPTH);
-            double a[R];
-#pragma unroll
-            for (int i = 0; i < R; ++i) a[i] = lane + 32 * i < d ? wring[slot][lane + 32 * i] : 0.0;
-            const double b = wring[slot][32 * R + 0], dj = wring[slot][32 * R + 1];
-            const double sj = wring[slot][32 * R + 2], yj = wring[slot][32 * R + 3];
-            const int j = jring[warp][slot];
-            __syncwarp();
-            issue(t + REPLICA_DEPTH, q1.k);           // reuses this slot
-            issue_perm(t + 2 * REPLICA_DEPTH, q2.k);
-            cp_async_commit();
-            q0 = adv(q0);
-            q1 = adv(q1);
-            q2 = adv(q2);
-            double acc = 0.0;
-#pragma unroll
-            for (int i = 0; i < R; ++i) acc += a[i] * (snap[lane + 32 * i] + pend[i]);
-            const double ga = warp_allsum(acc);
-            double raw = 0.0;
-            if (!coord_step(kind, p.lam, p.rho, yj, ga, p.quad * sj, b + dj, raw)) {
-                if (lane == 0) flag_error(st);
-                raw = 0.0;
-            }
-            const double step = damping * raw;
-            const double dn = step != 0.0 ? dj + step : dj;
-            if (lane == 0) {
-                dnext[j] = dn;
-                gacc += g_one(kind, p.lam, p.rho, yj, b + dn);
-            }
-            if (step != 0.0) {
-                const double f = p.quad * step;
-#pragma unroll
-                for (int i = 0; i < R; ++i) pend[i] += f * a[i];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-            if (pend[i] != 0.0) atomicAdd(&fold[lane + 32 * i], pend[i]);
-        __syncthreads();
-        if (threadIdx.x < d) {
-            const int r = threadIdx.x;
-            const double x = fold[r];
-            fold[r] = 0.0;
-            if (have_prev) {
-                double v = prev_own + prev_x;
-#pragma unroll
-                for (int c = 0; c < C; ++c)
-                    if (c != own) v += prev_oth[c];
-                snap[r] = v + x;
-            } else {
-                snap[r] += x;
-            }
-            prev_own = atomicAdd(vpad + ((int64_t)own * REPLICA_ROWS + r) * PAD_STRIDE, x);
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-                if (c != own) prev_oth[c] = ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
-            prev_x = x;
-            have_prev = true;
-        }
-#pragma unroll
-        for (int i = 0; i < R; ++i) pend[i] = 0.0;
-        __syncthreads();
-    }
-    cp_async_wait<0>();
-    // the last CTA to finish writes the shared view back (copies in order)
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&st->block_counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        for (int r = threadIdx.x; r < d; r += blockDim.x) {
-            double x = 0.0;
-            for (int c = 0; c < C; ++c)
-                x += ld_cg(vpad + ((int64_t)c * REPLICA_ROWS + r) * PAD_STRIDE);
-            view[r] = x;
-        }
         __syncthreads();
         if (threadIdx.x == 0) st->block_counter = 0;
     }
@@ -1559,66 +1323,35 @@ static int narrow_rows(int64_t d) {
     return 0;
 }
 
-// GLM_NARROW_KERNEL=v2: the replicated-copies narrow kernel (slower: the
-// reads of the other copies cost more L2 requests than the atomics it spreads)
-static bool narrow_v1_forced() {
-    const char *e = getenv("GLM_NARROW_KERNEL");
-    return !(e && strcmp(e, "v2") == 0);
-}
-// GLM_NARROW_COPIES=8: scd_replica2 spreads the view over 8 copies (default 1)
-static int narrow_copies() {
-    const char *e = getenv("GLM_NARROW_COPIES");
-    return e && strcmp(e, "8") == 0 ? REPLICA_COPIES : 1;
-}
-// GLM_NARROW_DELAY=2: consume the publish's atomic return two phases later
-static int narrow_delay2() {
-    const char *e = getenv("GLM_NARROW_DELAY");
-    return e && strcmp(e, "2") == 0 ? 1 : 0;
-}
-
 template <int R>
 static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, double *vpad,
                            cudaStream_t s) {
     count_launch();
     if (!async) {
         scd_seq_narrow<R><<<1, 32, 0, s>>>(p);
-    } else {
-        static int blocks_per_sm = 0, blocks_per_sm2 = 0;
-        if (!blocks_per_sm) {
-            GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                                       scd_replica<R>, 256, 0));
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-        }
-        const bool v1 = narrow_v1_forced();
-        const int copies = narrow_copies();
-        if (!v1 && !blocks_per_sm2) {
-            GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks_per_sm2, scd_replica2<R, 1>, 32 * REPLICA_WARPS, 0));
-            if (blocks_per_sm2 < 1) blocks_per_sm2 = 1;
-        }
-        constexpr int W = 8;
-        static_assert(W == REPLICA_WARPS, "one warp count for both narrow kernels");
-        int64_t cap = (int64_t)(v1 ? blocks_per_sm : blocks_per_sm2) * NUM_SMS;
-        if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
-        int64_t grid = budget / W;
-        if (grid < 1) grid = 1;
-        if (grid > cap) grid = cap;
-        const int64_t need = (p.m + W - 1) / W;      // at least one coordinate per warp
-        if (grid > need) grid = need < 1 ? 1 : need;
-        int64_t per = budget / (grid * W);
-        if (per < 1) per = 1;
-        if (per > 64) per = 64;
-        if (v1) {
-            narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
-            count_launch();
-            scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad, narrow_delay2());
-        } else {
-            narrow_pad2_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq, copies);
-            count_launch();
-            if (copies == 1) scd_replica2<R, 1><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
-            else scd_replica2<R, REPLICA_COPIES><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
-        }
+        GLM_CUDA_TRY(cudaGetLastError());
+        return GLM_OK;
     }
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                                   scd_replica<R>, 256, 0));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    constexpr int W = 8;
+    int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
+    if (cap > EPOCH_PARTIALS) cap = EPOCH_PARTIALS;
+    int64_t grid = budget / W;
+    if (grid < 1) grid = 1;
+    if (grid > cap) grid = cap;
+    const int64_t need = (p.m + W - 1) / W;      // at least one coordinate per warp
+    if (grid > need) grid = need < 1 ? 1 : need;
+    int64_t per = budget / (grid * W);
+    if (per < 1) per = 1;
+    if (per > 64) per = 64;
+    narrow_pad_kernel<<<1, 256, 0, s>>>(p.st, p.view0, p.view1, vpad, p.d, p.seq);
+    count_launch();
+    scd_replica<R><<<(int)grid, 32 * W, 0, s>>>(p, (int)per, vpad);
     GLM_CUDA_TRY(cudaGetLastError());
     return GLM_OK;
 }
