@@ -182,6 +182,11 @@ int glm_solver_destroy(glm_solver *s);
 /* Set the solver's permutation stream (PermutationGenerator(seed).state) and
  * damping (DampingState.delta) held in device memory. */
 int glm_solver_set_state(glm_solver *s, uint64_t gen_state, double damping, void *stream);
+/* Optional, once per CSC partition (outside any captured graph): build packed
+ * 16-byte per-coordinate records {start | count << 40, |a_j|^2} that the async
+ * epoch kernel then loads in one sector instead of the indptr pair and the
+ * norm.  Later solves on the same (indptr, sqnorms, n_cols) use them. */
+int glm_solver_prepare(glm_solver *s, const glm_matrix *A, void *stream);
 /* Asynchronous subtask: all attempts are enqueued on `stream`; outputs are
  * device arrays.  If args->max_attempts == 0 the call synchronises to run the
  * retry loop to completion and fills `res`; otherwise it enqueues exactly

@@ -133,6 +133,7 @@ SIGNATURES = {
     "glm_peer_destroy": (ctypes.c_int, [_P]),
     "glm_peer_stamps": (ctypes.c_int, [_P, _P]),
     "glm_peer_set_timeout": (ctypes.c_int, [_P, ctypes.c_double]),
+    "glm_solver_prepare": (ctypes.c_int, [_P, _P, _P]),
     "glm_peer_error": (ctypes.c_int, [_P, _P, ctypes.c_int]),
     "glm_round_turn": (ctypes.c_int, [_P, _P, ctypes.c_int, _c_dbl, _c_dbl, _P, _P, _c_i64, _P,
                                       _P, _c_i64, _P, _P, _P, _c_dbl, _c_dbl, ctypes.c_int, _P,

@@ -164,6 +164,7 @@ int glm_solver_destroy(glm_solver *s) {
     cudaFree(s->gpart);
     cudaFree(s->scratch);
     cudaFree(s->vpad);
+    cudaFree(s->meta);
     if (s->side) {
         cudaStreamSynchronize(s->side);
         cudaStreamDestroy(s->side);
@@ -224,6 +225,29 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     if (rc) { glm_solver_destroy(s); return rc; }
     GLM_CUDA_TRY(cudaDeviceSynchronize());
     *out = s;
+    return GLM_OK;
+}
+
+// Packed per-coordinate records of a CSC partition for the async epoch kernel
+// (one 16-byte load instead of the indptr pair and |a_j|^2; the records are
+// static for the matrix, so this runs once, outside any captured graph).
+int glm_solver_prepare(glm_solver *s, const glm_matrix *A, void *stream) {
+    if (!s || !A) return glm_set_error(GLM_USAGE, "null argument");
+    if (A->layout != GLM_CSC || !A->indptr || !A->sqnorms) return GLM_OK;   // dense: nothing
+    if (A->n_cols > s->max_coords) return glm_set_error(GLM_USAGE, "partition too large");
+    GLM_CUDA_TRY(cudaSetDevice(s->device));
+    if (!s->meta)
+        GLM_CUDA_TRY(cudaMalloc(&s->meta, sizeof(longlong2) * (size_t)(s->max_coords > 0 ? s->max_coords : 1)));
+    const int64_t m = A->n_cols;
+    if (m > 0) {
+        count_launch();
+        meta_build_kernel<<<grid_stride_blocks(m), 256, 0, (cudaStream_t)stream>>>(
+            A->indptr, A->sqnorms, m, s->meta);
+        GLM_CUDA_TRY(cudaGetLastError());
+    }
+    s->meta_indptr = A->indptr;
+    s->meta_sq = A->sqnorms;
+    s->meta_m = m;
     return GLM_OK;
 }
 
@@ -523,6 +547,7 @@ int glm_ctx_create(int device, int layout, int64_t n_rows, int64_t n_cols, const
     c->A.sqnorms = c->sq;
     int rc = launch_colwise(&c->A, 0, nullptr, c->sq, c->stream);
     if (!rc) rc = glm_solver_create(device, n_cols, n_rows, &c->solver);
+    if (!rc) rc = glm_solver_prepare(c->solver, &c->A, c->stream);   // packed records (CSC)
     if (!rc) {
         cudaError_t e2 = cudaStreamSynchronize(c->stream);
         if (e2 != cudaSuccess) rc = glm_set_cuda_error(e2, "ctx sync", __FILE__, __LINE__);

@@ -59,6 +59,7 @@ struct EpochParams {
     const int32_t *rows;
     const double *vals;
     const double *sq;
+    const longlong2 *meta;  // packed {start | count << 40, |a_j|^2} (CM bit 2) or NULL
     const double *base;
     const double *y;
     double *delta0, *delta1;
@@ -111,6 +112,11 @@ __device__ __forceinline__ void store_block_gsum(double g, double *gpart, SolveS
 // loaded once into registers (R elements per lane; longer columns stream the
 // tail), gathered against the shared view through L2, reduced with shuffles,
 // stepped on the group leader, and scattered with red.global.add.f64.
+// Packed coordinate record (glm_solver_prepare): start | count << 40 and the
+// bits of |a_j|^2; a count that does not fit 24 bits is the sentinel 2^24-1
+// (the kernel then reads indptr).
+constexpr int64_t META_CNT_SENTINEL = (1LL << 24) - 1;
+
 template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
@@ -154,21 +160,32 @@ __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
         const bool valid = k < p.m;
         const int j = valid ? __ldg(p.perm + k) : 0;
         int64_t lo = 0, hi = 0;
+        double sj = 0.0;
         if (valid) {
             if (DENSE) {
                 lo = (int64_t)j * p.d;
                 hi = lo + p.d;
+            } else if (CM & 4) {           // one 16-byte record: bounds and |a_j|^2
+                const longlong2 rec = __ldg(p.meta + j);
+                const int64_t cnt = (int64_t)((unsigned long long)rec.x >> 40);
+                lo = rec.x & ((1LL << 40) - 1);
+                hi = lo + cnt;
+                if (cnt == META_CNT_SENTINEL) {
+                    lo = __ldg(p.indptr + j);
+                    hi = __ldg(p.indptr + j + 1);
+                }
+                sj = __longlong_as_double(rec.y);
             } else {
                 lo = __ldg(p.indptr + j);
                 hi = __ldg(p.indptr + j + 1);
             }
         }
         // group leader prefetches the coordinate's metadata under the gather
-        double bj = 0.0, dj = 0.0, sj = 0.0, yj = 0.0;
+        double bj = 0.0, dj = 0.0, yj = 0.0;
         if (valid && gl == 0) {
             bj = __ldg(p.base + j);
             dj = dcur ? dcur[j] : 0.0;
-            sj = __ldg(p.sq + j);
+            if (!(CM & 4)) sj = __ldg(p.sq + j);
             if (p.y) yj = __ldg(p.y + j);
         }
         int rr[R];
@@ -1302,11 +1319,31 @@ static int launch_async_cm(const EpochParams &p, int lanes, int max_inflight, cu
 template <bool DENSE>
 static int launch_async(const EpochParams &p, int lanes, int max_inflight, int flags,
                         cudaStream_t s) {
+    if (!DENSE && p.meta) {          // a prepared partition: packed records
+        switch (flags & 3) {
+        case 1: return launch_async_cm<DENSE, 5>(p, lanes, max_inflight, s);
+        case 0: return launch_async_cm<DENSE, 4>(p, lanes, max_inflight, s);
+        default: break;
+        }
+    }
     switch (flags & 3) {
     case 1: return launch_async_cm<DENSE, 1>(p, lanes, max_inflight, s);
     case 2: return launch_async_cm<DENSE, 2>(p, lanes, max_inflight, s);
     case 3: return launch_async_cm<DENSE, 3>(p, lanes, max_inflight, s);
     default: return launch_async_cm<DENSE, 0>(p, lanes, max_inflight, s);
+    }
+}
+
+__global__ void meta_build_kernel(const int64_t *indptr, const double *sq, int64_t m,
+                                  longlong2 *meta) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = indptr[j], cnt = indptr[j + 1] - lo;
+        const bool fits = cnt < META_CNT_SENTINEL && lo >= 0 && lo < (1LL << 40);
+        longlong2 r;
+        r.x = fits ? (lo | (cnt << 40)) : (META_CNT_SENTINEL << 40);
+        r.y = __double_as_longlong(sq[j]);
+        meta[j] = r;
     }
 }
 
@@ -1617,6 +1654,9 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     ep.rows = A->rows;
     ep.vals = A->vals;
     ep.sq = A->sqnorms;
+    // packed records when this partition was prepared (glm_solver_prepare)
+    ep.meta = (!dense && s->meta && s->meta_indptr == A->indptr && s->meta_sq == A->sqnorms &&
+               s->meta_m == m) ? s->meta : nullptr;
     ep.base = a->base;
     ep.y = a->coord_target;
     ep.delta0 = s->delta[0];
@@ -2037,6 +2077,7 @@ int chunk_enqueue(glm_solver *s, const StreamSolve &a, const ChunkJob &c, cudaSt
     ep.rows = A->rows;
     ep.vals = A->vals;
     ep.sq = A->sqnorms;
+    ep.meta = nullptr;
     ep.base = a.base + c.lo;
     ep.y = a.y ? a.y + c.lo : nullptr;
     ep.delta0 = a.dfull + c.lo;     // read: the accepted state (st->dc == 0)

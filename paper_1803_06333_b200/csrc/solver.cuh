@@ -39,6 +39,12 @@ struct glm_solver {
     const double *sq_src = nullptr;       // mean |a|^2 cache (narrow dense budget)
     int64_t sq_n = -1;
     double sq_mean = 1.0;
+    // packed coordinate records of a prepared CSC partition (glm_solver_prepare):
+    // {start | count << 40, |a_j|^2} — 16 bytes, one sector per coordinate
+    longlong2 *meta = nullptr;
+    const int64_t *meta_indptr = nullptr;
+    const double *meta_sq = nullptr;
+    int64_t meta_m = -1;
 };
 
 namespace glm {

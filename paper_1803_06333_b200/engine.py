@@ -158,6 +158,8 @@ class _Worker:
         self.gen = _GenView(derive_seed(engine.config.seed, seed_index))
         self.damping = _DampView()
         self.solver.set_state(self.gen.state, 1.0, engine.stream)
+        if engine.mode == L.MODE_ASYNC and self.data.layout == L.CSC and self.m > 0:
+            self.solver.prepare(self.data, engine.stream)     # packed coordinate records
         self.gsum_ok = False        # solver's cached g-sum matches alpha[cols]
         self.coord_target = None
         ct = engine.spec.coord_target

@@ -236,6 +236,12 @@ class DeviceSolver:
                                              float(damping), _D().sptr(stream)),
                 "glm_solver_set_state")
 
+    def prepare(self, dm, stream=None):
+        """Packed per-coordinate records of a CSC partition for the async
+        epoch kernel (glm_solver_prepare); a no-op for dense data."""
+        L.check(L.lib().glm_solver_prepare(self.handle, ctypes.byref(dm.struct),
+                                           _D().sptr(stream)), "glm_solver_prepare")
+
     def solve(self, dm, spec, *, lin, cnst, base, quad, epochs, mode, delta_out, dv_out,
               coord_target=None, reset_damping=False, max_attempts=0, group_lanes=0,
               max_inflight=0, accumulate=False, flags=0, stream=None, peer=None):
