@@ -209,7 +209,7 @@ int glm_solver_create(int device, int64_t max_coords, int64_t max_rows, glm_solv
     chk(cudaMalloc(&s->partials, sizeof(double) * 3 * 8 * NUM_SMS));
     chk(cudaMalloc(&s->gpart, sizeof(double) * 16 * NUM_SMS));
     chk(cudaMalloc(&s->scratch, REDUCE_SCRATCH_BYTES));
-    chk(cudaMalloc(&s->vpad, sizeof(double) * 256 * PAD_STRIDE));
+    chk(cudaMalloc(&s->vpad, sizeof(double) * NARROW_MAX_ROWS * PAD_STRIDE));
     if (e == cudaSuccess) {
         chk(cudaMemset(s->perm_mem, 0, pb));
         chk(cudaMemset(s->scratch, 0, REDUCE_SCRATCH_BYTES));

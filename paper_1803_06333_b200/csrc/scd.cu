@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(32) scd_seq_narrow(EpochParams p) {
 // (address bits 10+); contiguous, all CTAs' atomics would queue on the one
 // or two slices holding the view's 224 bytes.
 constexpr int PAD_STRIDE = 128;
+constexpr int NARROW_MAX_ROWS = 1024;   // dense views kept in registers (32 per lane)
 
 __global__ void narrow_pad_kernel(const SolveState *st, const double *view0, const double *view1,
                                   double *vpad, int64_t d, int64_t seq) {
@@ -390,7 +391,11 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
     for (int i = 0; i < R; ++i) pend[i] = 0.0;
     const int64_t per_cta = (int64_t)nwarp * per_phase;
     const int64_t stride = (int64_t)gridDim.x * per_cta;
-    double prev_old = 0.0, prev_x = 0.0;   // row threadIdx.x: the last publish
+    // rows threadIdx.x + 256 q (q < RPT) of the view: their last publish
+    constexpr int RPT = (32 * R + 255) / 256;
+    double prev_old[RPT], prev_x[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) prev_old[q] = prev_x[q] = 0.0;
     bool have_prev = false;
     // This warp's coordinates: position t -> k(t) = base + (t / P) * stride +
     // t % P.  Two-stage software pipeline: the permutation entry of t + 2 and
@@ -451,15 +456,18 @@ __global__ void __launch_bounds__(256) scd_replica(EpochParams p, int per_phase,
         for (int i = 0; i < R; ++i)
             if (pend[i] != 0.0) atomicAdd(&fold[lane + 32 * i], pend[i]);
         __syncthreads();
-        if (threadIdx.x < p.d) {
-            const int r = threadIdx.x;
-            const double x = fold[r];
-            fold[r] = 0.0;
-            snap[r] = have_prev ? prev_old + prev_x + x : snap[r] + x;
-            prev_old = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
-            prev_x = x;
-            have_prev = true;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int r = threadIdx.x + 256 * q;
+            if (r < p.d) {
+                const double x = fold[r];
+                fold[r] = 0.0;
+                snap[r] = have_prev ? prev_old[q] + prev_x[q] + x : snap[r] + x;
+                prev_old[q] = atomicAdd(vpad + (int64_t)r * PAD_STRIDE, x);
+                prev_x[q] = x;
+            }
         }
+        have_prev = true;
 #pragma unroll
         for (int i = 0; i < R; ++i) pend[i] = 0.0;
         __syncthreads();
@@ -1357,6 +1365,8 @@ static int narrow_rows(int64_t d) {
     if (d <= 64) return 2;
     if (d <= 128) return 4;
     if (d <= 256) return 8;
+    if (d <= 512) return 16;      // C1 dual: 500 rows, 16 registers per lane
+    if (d <= NARROW_MAX_ROWS) return 32;
     return 0;
 }
 
@@ -1399,7 +1409,9 @@ static int launch_narrow(const EpochParams &p, bool async, int64_t budget, doubl
     case 1: return launch_narrow_t<1>(p, async, budget, vpad, s);
     case 2: return launch_narrow_t<2>(p, async, budget, vpad, s);
     case 4: return launch_narrow_t<4>(p, async, budget, vpad, s);
-    default: return launch_narrow_t<8>(p, async, budget, vpad, s);
+    case 8: return launch_narrow_t<8>(p, async, budget, vpad, s);
+    case 16: return launch_narrow_t<16>(p, async, budget, vpad, s);
+    default: return launch_narrow_t<32>(p, async, budget, vpad, s);
     }
 }
 

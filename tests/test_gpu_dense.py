@@ -1,5 +1,5 @@
 """GPU parity of the dense column-major layout (C1 ridge, C3 HIGGS-shaped SVM):
-the narrow-column kernels (d <= 256: register-resident sequential warp,
+the narrow-column kernels (d <= 1024: register-resident sequential warp,
 CTA-replica asynchronous kernel) and the wide dense path, vs the CPU oracle
 run on the same matrix in CSC form."""
 
@@ -34,7 +34,7 @@ def _csc(dense):
     return oracle.OMatrix(d, indptr, rows, dense.T.reshape(-1).copy())
 
 
-@pytest.mark.parametrize("d", [28, 60, 200])
+@pytest.mark.parametrize("d", [28, 60, 200, 500, 900])
 def test_narrow_dense_sequential_matches_oracle(d):
     A = _higgs(3_000, d, d)
     m = g.DenseColumnMatrix(A)
@@ -100,6 +100,23 @@ def test_narrow_dense_async_delta_v_consistent():
     sub = g.LocalSubproblem(spec=spec, lin=lin, quad=1 / 20.0, const=0.0,
                             base=spec.init_alpha(), data=m, col_ids=np.arange(m.n_cols))
     res = g.damped_solve(sub, g.PermutationGenerator(3), 3, n_threads=8)
+    assert res.final_subproblem_value < res.initial_subproblem_value
+    assert np.all(np.diff(res.epoch_values) <= 0)
+    dv = oracle.matvec(om, np.asarray(res.delta_alpha))
+    assert np.max(np.abs(np.asarray(res.delta_v) - dv)) < 1e-9 * max(1.0, np.max(np.abs(dv)))
+
+
+@pytest.mark.parametrize("d", [500, 900])
+def test_narrow_async_wide_views(d):
+    """16 / 32 view rows per lane (C1 dual's 500-row view): the async replica
+    kernel keeps Delta v = B delta and decreases the subproblem."""
+    A = _higgs(20_000, d, d + 1)
+    m = g.DenseColumnMatrix(A)
+    om = _csc(A)
+    spec = g.ObjectiveSpec("dual_l2_svm", 5.0, m.n_cols, m.n_rows)
+    sub = g.LocalSubproblem(spec=spec, lin=np.zeros(d), quad=1 / 5.0, const=0.0,
+                            base=spec.init_alpha(), data=m, col_ids=np.arange(m.n_cols))
+    res = g.damped_solve(sub, g.PermutationGenerator(4), 3, n_threads=8)
     assert res.final_subproblem_value < res.initial_subproblem_value
     assert np.all(np.diff(res.epoch_values) <= 0)
     dv = oracle.matvec(om, np.asarray(res.delta_alpha))
