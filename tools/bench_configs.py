@@ -290,7 +290,8 @@ def c4(args):
     res = {"config": "C4", "workload": f"lasso (primal), sparse {n_ex}x{n_feat}, "
                                        f"{per_col} nnz/feature, lambda={lam}", "nnz": nnz}
     eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode="async",
-                   sync_solves=False)
+                   sync_solves=False, cache_flags=args.cache_flags)
+    res["cache_flags"] = args.cache_flags
     ms_all = []
     objs = []
     for r in range(args.rounds):
@@ -395,6 +396,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", choices=("c1", "c1d", "c2", "c2p", "c2cpu", "c3", "c4", "c5"))
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cache-flags", type=int, default=0,
+                    help="C4: glm_solve_args.flags cache bits (1 view via L1, 2 stream evict-first / "
+                         "view evict-last, 3 both)")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--lam", type=float, default=None)
     ap.add_argument("--rounds", type=int, default=10)
