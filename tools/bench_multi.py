@@ -86,8 +86,7 @@ def c3(args, rank, world):
     spec = g.ObjectiveSpec("dual_l2_svm", lam, n_tot, d)
     cfg = g.HierarchyConfig(nodes=world, seed=0, epochs=1)
     kw = dict(reducer=NcclReducer(), node_index=rank, n_total=n_tot) if world > 1 else {}
-    eng = g.Engine(dm, spec, cfg, mode="async", sync_solves=False, retry_budget=0,
-                   cache_flags=3, **kw)    # C4: stream evict-first, view evict-last + L1
+    eng = g.Engine(dm, spec, cfg, mode="async", sync_solves=False, retry_budget=0, **kw)
     for _ in range(2):
         eng.outer_round()
     eng.reset()
