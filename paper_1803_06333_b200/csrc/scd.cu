@@ -1330,8 +1330,9 @@ static int launch_async(const EpochParams &p, int lanes, int max_inflight, int f
     if (!DENSE && p.meta) {          // a prepared partition: packed records
         switch (flags & 3) {
         case 1: return launch_async_cm<DENSE, 5>(p, lanes, max_inflight, s);
-        case 0: return launch_async_cm<DENSE, 4>(p, lanes, max_inflight, s);
-        default: break;
+        case 2: return launch_async_cm<DENSE, 6>(p, lanes, max_inflight, s);
+        case 3: return launch_async_cm<DENSE, 7>(p, lanes, max_inflight, s);
+        default: return launch_async_cm<DENSE, 4>(p, lanes, max_inflight, s);
         }
     }
     switch (flags & 3) {
