@@ -225,7 +225,7 @@ int glm_argsort_u32(const uint32_t *keys, int64_t n, int32_t *perm, void *temp,
  * PermutationGenerator(state).permute(n) (solver.py:86-89) and
  * keys_to_permutation(generate_keys(seed, n)) (pipeline.py:29-78).  The keys
  * are regenerated in both passes, never stored.  temp: glm_argsort_temp_bytes(n)
- * bytes, zeroed by the call. */
+ * bytes (its counters are zeroed by the call). */
 int glm_perm(uint64_t state, int64_t n, int32_t *perm, void *temp, size_t temp_bytes,
              void *stream);
 int glm_chunk_perm(uint64_t seed, int64_t n, int32_t *perm, void *temp, size_t temp_bytes,

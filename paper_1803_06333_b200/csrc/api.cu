@@ -301,7 +301,7 @@ int glm_argsort_u32(const uint32_t *keys, int64_t n, int32_t *perm, void *temp,
                     size_t temp_bytes, void *stream) {
     if (temp_bytes < perm_scratch_bytes(n))
         return glm_set_error(GLM_USAGE, "argsort scratch too small");
-    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_bytes(n), S(stream)));
+    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_head_bytes(n), S(stream)));
     PermScratch ps = carve_perm_scratch(temp, n, n);
     return array_perm(keys, n, perm, ps, S(stream));
 }
@@ -312,7 +312,7 @@ int glm_perm(uint64_t state, int64_t n, int32_t *perm, void *temp, size_t temp_b
     if (rc) return rc;
     if (temp_bytes < perm_scratch_bytes(n))
         return glm_set_error(GLM_USAGE, "permutation scratch too small");
-    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_bytes(n), S(stream)));
+    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_head_bytes(n), S(stream)));
     PermScratch ps = carve_perm_scratch(temp, n, n);
     return stream_perm(nullptr, state ? state : 0x9E3779B97F4A7C15ULL, 0, n, perm, ps,
                        S(stream));
@@ -324,7 +324,7 @@ int glm_chunk_perm(uint64_t seed, int64_t n, int32_t *perm, void *temp, size_t t
     if (rc) return rc;
     if (temp_bytes < perm_scratch_bytes(n))
         return glm_set_error(GLM_USAGE, "permutation scratch too small");
-    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_bytes(n), S(stream)));
+    GLM_CUDA_TRY(cudaMemsetAsync(temp, 0, perm_scratch_head_bytes(n), S(stream)));
     PermScratch ps = carve_perm_scratch(temp, n, n);
     return chunk_perm(seed, n, perm, ps, S(stream));
 }

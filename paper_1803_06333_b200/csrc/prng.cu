@@ -16,20 +16,26 @@
 // base state is derive_seed(seed, block).
 //
 // The stable argsort never materialises the keys.  Two variants, same order:
-//  * row counts (generated keys, n <= 2^21 — every partition and chunk of the
-//    configs): pass 1 histograms each 4096-key block's top `nb2` bits (~512
-//    keys per bucket) in shared memory, writes one count row per block and
-//    saves every thread's start state; a column scan turns the rows into
-//    per-(block, bucket) offsets; pass 2 re-walks the keys from the saved
-//    states and scatters (key<<32 | index) through shared-memory cursors; one
-//    CTA per bucket spreads its pairs over 256 sub-buckets (the next 8 key
-//    bits) in shared memory and each thread insertion-sorts one sub-bucket.
-//    No global atomics; 4 kernels.
+//  * bucket regions (generated keys, n <= 2^21 — every partition and chunk of
+//    the configs): 2 kernels.  Pass 1 (one CTA per 4096-key block) walks its
+//    keys twice from registers: a shared-memory histogram of the top `nb2`
+//    bits (<= 512 keys per bucket on average), one global atomicAdd per
+//    non-empty bucket to reserve a run in that bucket's fixed 1024-pair
+//    region, then the (key<<32 | index) pairs go to their runs; the last CTA
+//    (ticket) scans the bucket totals into output offsets.  Pass 2 (one CTA
+//    per bucket) spreads its pairs over 256 sub-buckets (the next 8 key bits)
+//    in shared memory, each thread insertion-sorts one, and the CTA writes
+//    its slice of the permutation.  The order inside a region depends on the
+//    atomics, the sorted result does not (pairs are unique).  A bucket beyond
+//    its region spills to an overflow list and is sorted by a slow path.
 //  * global buckets (larger n, and argsort of caller keys): pass 1 histograms
 //    the top `nb` bits (~8 keys per bucket) with global atomics, a two-kernel
 //    scan gives bucket offsets, pass 2 regenerates the keys and scatters, and
 //    a warp per 32 buckets insertion-sorts them in shared memory.  Oversized
 //    bucket groups fall back to an in-place sort in global memory.
+// Block start states: M^(4096 b) s0 from a table of the first 512 block
+// jumps (one warp matrix-vector product instead of a chain of ~20 dependent
+// jump-table loads); the attempt offset, when not 0, is one warp_jump.
 #include <algorithm>
 #include <mutex>
 
@@ -44,9 +50,12 @@ constexpr int KEYS_PER_BLOCK = PERM_THREADS * KPT;  // 4096 == pipeline.KEY_BLOC
 
 __device__ uint64_t d_jump_cols[64 * 64];            // [i][b]: column b of M^(2^i)
 __device__ uint64_t d_thread_jump[PERM_THREADS * 64];  // [b][t]: column b of M^(16 t)
+constexpr int BLK_JUMPS = 512;                        // 2^21 keys / 4096
+__device__ uint64_t d_blk_jump[BLK_JUMPS * 64];       // [blk][b]: column b of M^(4096 blk)
 
 static uint64_t h_jump_cols[64 * 64];
 static uint64_t h_thread_jump[PERM_THREADS * 64];
+static uint64_t h_blk_jump[BLK_JUMPS * 64];
 static std::once_flag h_jump_once;
 static bool d_jump_ready[64];
 static std::mutex d_jump_mutex;
@@ -79,6 +88,12 @@ static void build_host_jump() {
             for (int k = 0; k < KPT; ++k) s = xs_step(s);
         }
     }
+    // block matrices M^(4096 blk) = (M^4096)^blk, M^4096 = M^(2^12)
+    const uint64_t *m4096 = h_jump_cols + 12 * 64;
+    for (int b = 0; b < 64; ++b) h_blk_jump[b] = 1ULL << b;
+    for (int k = 1; k < BLK_JUMPS; ++k)
+        for (int b = 0; b < 64; ++b)
+            h_blk_jump[k * 64 + b] = mat_apply(m4096, h_blk_jump[(k - 1) * 64 + b]);
 }
 
 uint64_t host_jump(uint64_t state, uint64_t steps) {
@@ -96,6 +111,7 @@ int ensure_device_tables() {
     std::call_once(h_jump_once, build_host_jump);
     GLM_CUDA_TRY(cudaMemcpyToSymbol(d_jump_cols, h_jump_cols, sizeof(h_jump_cols)));
     GLM_CUDA_TRY(cudaMemcpyToSymbol(d_thread_jump, h_thread_jump, sizeof(h_thread_jump)));
+    GLM_CUDA_TRY(cudaMemcpyToSymbol(d_blk_jump, h_blk_jump, sizeof(h_blk_jump)));
     GLM_CUDA_TRY(cudaDeviceSynchronize());
     if (dev < 64) d_jump_ready[dev] = true;
     return GLM_OK;
@@ -139,6 +155,17 @@ __device__ __forceinline__ uint64_t warp_jump(uint64_t state, uint64_t steps) {
     }
 }
 
+// M^(4096 blk) state for the first BLK_JUMPS blocks: every lane applies two
+// columns (one load each), one XOR reduction; later blocks take warp_jump.
+__device__ __forceinline__ uint64_t block_jump(uint64_t state, int64_t blk) {
+    if (blk >= BLK_JUMPS) return warp_jump(state, (uint64_t)blk * KEYS_PER_BLOCK);
+    const int lane = threadIdx.x & 31;
+    const uint64_t *c = d_blk_jump + blk * 64;
+    const uint64_t c0 = c[lane], c1 = c[lane + 32];
+    return xor_reduce_warp((((state >> lane) & 1) ? c0 : 0ULL) ^
+                           (((state >> (lane + 32)) & 1) ? c1 : 0ULL));
+}
+
 __device__ __forceinline__ uint64_t thread_apply(uint64_t state) {
     const uint64_t *c = d_thread_jump + threadIdx.x;
     uint64_t y = 0;
@@ -171,7 +198,7 @@ struct StreamKeys {       // PermutationGenerator stream at attempt offset
     __device__ __forceinline__ bool skip() const { return st && st->done; }
     __device__ __forceinline__ uint64_t block_base() const {
         const uint64_t s0 = state_ptr ? *state_ptr : state;
-        return warp_jump(s0, offset + (uint64_t)blockIdx.x * KEYS_PER_BLOCK);
+        return block_jump(offset ? warp_jump(s0, offset) : s0, blockIdx.x);
     }
 };
 
@@ -373,152 +400,15 @@ __global__ void __launch_bounds__(BS_WARPS * 32) bucket_sort_kernel(const SolveS
     }
 }
 
-// ------------------------------------------------- row-count variant (v2)
+// ------------------------------------------------- bucket-region variant
 constexpr int V2_MAX_LOG = 21;
+constexpr int BCAP = 1024;             // pairs per bucket region (<= 512 expected)
 constexpr int BS2_THREADS = 256;
-constexpr int BS2_CAP = 1024;          // pairs per bucket sorted in shared memory
-constexpr int CS_WARPS = 32;
 
 __device__ __forceinline__ uint32_t bucket_of(uint32_t k, int nb) {
     return nb ? k >> (32 - nb) : 0u;
 }
 
-template <class Src>
-__global__ void __launch_bounds__(PERM_THREADS) hist2_kernel(Src src, int64_t n, int nb,
-                                                             uint32_t *counts, uint64_t *tstate) {
-    if (src.skip()) return;
-    tl_start(TL_PERM_FIRST);
-    extern __shared__ uint32_t h2[];
-    const int NB = 1 << nb;
-    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) h2[i] = 0;
-    __syncthreads();
-    for_keys(src, n, [&](int64_t, uint32_t k) { atomicAdd(h2 + bucket_of(k, nb), 1u); }, tstate);
-    __syncthreads();
-    uint32_t *row = counts + (size_t)blockIdx.x * NB;
-    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) row[i] = h2[i];
-    tl_end(TL_PERM_FIRST);
-}
-
-// Grid NB/32 CTAs of 32 warps; lane = bucket, warp = a contiguous segment of
-// the count rows.  Rows become exclusive offsets within the bucket; tot[b] =
-// bucket total; the last CTA writes boff = exclusive scan of tot.
-__global__ void __launch_bounds__(CS_WARPS * 32) colscan2_kernel(const SolveState *st,
-                                                                 uint32_t *counts, int nblk,
-                                                                 int nb, uint32_t *tot,
-                                                                 uint32_t *boff,
-                                                                 uint32_t *ticket) {
-    if (st && st->done) return;
-    tl_start(TL_SCAN);
-    __shared__ uint32_t s_part[CS_WARPS][32];
-    __shared__ uint32_t s_warp[CS_WARPS];
-    __shared__ bool s_last;
-    const int NB = 1 << nb;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int b = blockIdx.x * 32 + lane;
-    const int r0 = (int)((int64_t)nblk * w / CS_WARPS);
-    const int r1 = (int)((int64_t)nblk * (w + 1) / CS_WARPS);
-    uint32_t sum = 0;
-    if (b < NB) {
-        for (int r = r0; r < r1; r += 8) {
-            uint32_t c[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) c[j] = r + j < r1 ? counts[(size_t)(r + j) * NB + b] : 0u;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sum += c[j];
-        }
-    }
-    s_part[w][lane] = sum;
-    __syncthreads();
-    if (w == 0) {
-        uint32_t acc = 0;
-#pragma unroll
-        for (int j = 0; j < CS_WARPS; ++j) {
-            const uint32_t x = s_part[j][lane];
-            s_part[j][lane] = acc;
-            acc += x;
-        }
-        if (b < NB) tot[b] = acc;
-    }
-    __syncthreads();
-    if (b < NB) {
-        uint32_t run = s_part[w][lane];
-        for (int r = r0; r < r1; r += 8) {
-            uint32_t c[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) c[j] = r + j < r1 ? counts[(size_t)(r + j) * NB + b] : 0u;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (r + j < r1) {
-                    counts[(size_t)(r + j) * NB + b] = run;
-                    run += c[j];
-                }
-        }
-    }
-    __threadfence();
-    __syncthreads();
-    tl_end(TL_SCAN);
-    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // exclusive scan of the NB (<= 4096) totals: `per` (<= 4) consecutive per thread
-    const int per = (NB + CS_WARPS * 32 - 1) / (CS_WARPS * 32);
-    const int i0 = threadIdx.x * per;
-    uint32_t v[4];
-    uint32_t mine = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        v[j] = j < per && i0 + j < NB ? __ldcg(tot + i0 + j) : 0u;
-        mine += v[j];
-    }
-    uint32_t inc = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_warp[w] = inc;
-    __syncthreads();
-    uint32_t pre = inc - mine;
-    for (int j = 0; j < w; ++j) pre += s_warp[j];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (j < per && i0 + j < NB) {
-            boff[i0 + j] = pre;
-            pre += v[j];
-        }
-    if (threadIdx.x == CS_WARPS * 32 - 1) {
-        boff[NB] = pre;
-        *ticket = 0;              // ready for the next permutation
-    }
-}
-
-template <class Src>
-__global__ void __launch_bounds__(PERM_THREADS) scatter2_kernel(Src src, int64_t n, int nb,
-                                                                const uint32_t *counts,
-                                                                const uint32_t *boff,
-                                                                const uint64_t *tstate,
-                                                                uint64_t *pairs) {
-    if (src.skip()) return;
-    tl_start(TL_SCATTER);
-    extern __shared__ uint32_t cur2[];
-    const int NB = 1 << nb;
-    const uint32_t *row = counts + (size_t)blockIdx.x * NB;
-    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) cur2[i] = boff[i] + row[i];
-    __syncthreads();
-    walk_keys(tstate[(size_t)blockIdx.x * PERM_THREADS + threadIdx.x], n,
-              [&](int64_t q, uint32_t k) {
-        const uint32_t pos = atomicAdd(cur2 + bucket_of(k, nb), 1u);
-        pairs[pos] = ((uint64_t)k << 32) | (uint32_t)q;
-    });
-    __syncthreads();
-    tl_end(TL_SCATTER);
-}
-
-// One CTA per bucket (~512 pairs): a counting pass on the next 8 key bits
-// spreads the pairs over 256 sub-buckets in shared memory (~2 pairs each),
-// then thread t insertion-sorts sub-bucket t by (key, index) — numpy's stable
-// order — and the CTA writes its slice of the permutation coalesced.
 __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_warp) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t inc = x;
@@ -534,24 +424,101 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_
     return pre;
 }
 
-__global__ void __launch_bounds__(BS2_THREADS) bsort2_kernel(const SolveState *st,
-                                                             uint64_t *pairs,
-                                                             const uint32_t *boff, int nb,
-                                                             int32_t *perm) {
+// Pass 1.  ctl: [0] ticket, [1] overflow count, [2] overflow total (for pass 2);
+// cnt: per-bucket totals.  Both are zero between uses (the last CTA resets).
+template <class Src>
+__global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
+    Src src, int64_t n, int nb, uint32_t *cnt, uint32_t *boff, uint32_t *ctl, uint64_t *region,
+    uint64_t *ovf, uint32_t *ovf_b) {
+    if (src.skip()) return;
+    tl_start(TL_PERM_FIRST);
+    extern __shared__ uint32_t h3[];
+    __shared__ uint64_t s_base;
+    __shared__ uint32_t s_warp[PERM_THREADS / 32];
+    __shared__ bool s_last;
+    const int NB = 1 << nb;
+    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) h3[i] = 0;
+    if (threadIdx.x < 32) {
+        const uint64_t b = src.block_base();
+        if (threadIdx.x == 0) s_base = b;
+    }
+    __syncthreads();
+    const int64_t q0 = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (int64_t)threadIdx.x * KPT;
+    const uint64_t s = q0 < n ? thread_apply(s_base) : 0ULL;
+    walk_keys(s, n, [&](int64_t, uint32_t k) { atomicAdd(h3 + bucket_of(k, nb), 1u); });
+    __syncthreads();
+    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) {   // reserve this block's runs
+        const uint32_t c = h3[i];
+        h3[i] = c ? atomicAdd(cnt + i, c) : 0u;
+    }
+    __syncthreads();
+    walk_keys(s, n, [&](int64_t q, uint32_t k) {
+        const uint32_t b = bucket_of(k, nb);
+        const uint32_t pos = atomicAdd(h3 + b, 1u);
+        const uint64_t pr = ((uint64_t)k << 32) | (uint32_t)q;
+        if (pos < (uint32_t)BCAP) {
+            region[(size_t)b * BCAP + pos] = pr;
+        } else {
+            const uint32_t o = atomicAdd(ctl + 1, 1u);
+            ovf[o] = pr;
+            ovf_b[o] = b;
+        }
+    });
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ctl, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {       // every block's reservations are in: bucket output offsets
+        __threadfence();
+        const int per = (NB + PERM_THREADS - 1) / PERM_THREADS;      // <= 16
+        const int i0 = threadIdx.x * per;
+        uint32_t c[16];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            c[j] = j < per && i0 + j < NB ? __ldcg(cnt + i0 + j) : 0u;
+            mine += c[j];
+        }
+        uint32_t pre = block_excl_scan_256(mine, s_warp);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < per && i0 + j < NB) {
+                boff[i0 + j] = pre;
+                pre += c[j];
+                cnt[i0 + j] = 0;                 // ready for the next permutation
+            }
+        if (threadIdx.x == PERM_THREADS - 1) boff[NB] = pre;
+        if (threadIdx.x == 0) {
+            ctl[2] = atomicExch(ctl + 1, 0u);
+            ctl[0] = 0;
+        }
+    }
+    tl_end(TL_PERM_FIRST);
+}
+
+// Pass 2: one CTA per bucket.  A counting pass on the next 8 key bits spreads
+// the pairs over 256 sub-buckets in shared memory (~2 pairs each), thread t
+// insertion-sorts sub-bucket t by (key, index) — numpy's stable order — and
+// the CTA writes its slice of the permutation coalesced.
+__global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
+    const SolveState *st, const uint64_t *region, const uint32_t *boff, int nb,
+    const uint32_t *ctl, const uint64_t *ovf, const uint32_t *ovf_b, uint64_t *tmp,
+    int32_t *perm) {
     if (st && st->done) return;
     tl_start(TL_PERM_LAST);
-    __shared__ uint64_t s_in[BS2_CAP], s_out[BS2_CAP];
+    __shared__ uint64_t s_in[BCAP], s_out[BCAP];
     __shared__ uint32_t s_cur[BS2_THREADS];
     __shared__ uint32_t s_warp[BS2_THREADS / 32];
     const uint32_t lo = boff[blockIdx.x], hi = boff[blockIdx.x + 1];
     const int cnt = (int)(hi - lo);
+    const uint64_t *src = region + (size_t)blockIdx.x * BCAP;
     const int t = threadIdx.x;
-    if (cnt <= BS2_CAP) {
+    if (cnt <= BCAP) {
         const int sh = 24 - nb;                    // the 8 key bits below the bucket bits
         s_cur[t] = 0;
         __syncthreads();
         for (int i = t; i < cnt; i += BS2_THREADS) {
-            const uint64_t p = pairs[lo + i];
+            const uint64_t p = src[i];
             s_in[i] = p;
             atomicAdd(s_cur + ((uint32_t)(p >> 32) >> sh & 255u), 1u);
         }
@@ -568,29 +535,29 @@ __global__ void __launch_bounds__(BS2_THREADS) bsort2_kernel(const SolveState *s
         insertion_sort(s_out + ex, (int)c);
         __syncthreads();
         for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)s_out[i];
-    } else {                      // never seen with uniform keys; same order, slowly
-        if (t == 0) insertion_sort(pairs + lo, cnt);
+    } else {            // the bucket outgrew its region: region + overflow list, slowly
+        for (int i = t; i < BCAP; i += BS2_THREADS) tmp[lo + i] = src[i];
+        if (t == 0) {
+            int w = BCAP;
+            const uint32_t no = ctl[2];
+            for (uint32_t o = 0; o < no; ++o)
+                if (ovf_b[o] == blockIdx.x) tmp[lo + w++] = ovf[o];
+        }
         __syncthreads();
-        for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)pairs[lo + i];
+        if (t == 0) insertion_sort(tmp + lo, cnt);
+        __syncthreads();
+        for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)tmp[lo + i];
     }
     tl_end(TL_PERM_LAST);
 }
 
-static int v2_bits(int64_t n) {       // ~512 keys per bucket, <= 4096 buckets
+static int v2_bits(int64_t n) {       // <= 512 keys per bucket on average, <= 4096 buckets
     int lg = 0;
     while ((1LL << lg) < n) ++lg;
     int nb = lg - 9;
     if (nb < 0) nb = 0;
     if (nb > 12) nb = 12;
     return nb;
-}
-
-static size_t v2_bytes(int64_t capacity) {
-    const int64_t c = std::min<int64_t>(capacity > 0 ? capacity : 1, 1LL << V2_MAX_LOG);
-    const int64_t nblk = (c + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
-    const int64_t NB = 1LL << v2_bits(c);
-    return sizeof(uint32_t) * (size_t)(nblk * NB + 2 * NB + 2 + 64) +
-           sizeof(uint64_t) * (size_t)(nblk * PERM_THREADS) + 256;
 }
 
 // ---------------------------------------------------------------------------
@@ -603,41 +570,65 @@ int bucket_bits(int64_t n) {
     return nb;
 }
 
-size_t perm_scratch_bytes(int64_t n) {
-    const int64_t nbk = 1LL << bucket_bits(n);
-    const size_t a = sizeof(uint64_t) * (size_t)(n > 0 ? n : 1);             // pairs
-    const size_t h = sizeof(uint32_t) * (size_t)(3 * nbk + 1 + nbk / SCAN_TILE + 2);
-    return a + h + 1024 + v2_bytes(n) + 256;
+// Layout (offsets depend only on `capacity`, so the zeroed counters stay in
+// place across calls with different n; every kernel re-zeroes what it used):
+//   head: hist | offs | cursor | tile sums | ctl[64] | cnt | boff   (zeroed once)
+//   bulk: pairs[capacity] | bucket regions | overflow pairs | overflow buckets
+namespace {
+struct Layout {
+    size_t hist, offs, cursor, flags, ctl, cnt, boff, head;
+    size_t pairs, region, ovf, ovf_b, total;
+    int64_t nbk_cap, nb2_cap, c2;
+};
+size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
+Layout layout(int64_t capacity) {
+    Layout L{};
+    const int64_t cap = capacity > 0 ? capacity : 1;
+    L.nbk_cap = 1LL << bucket_bits(cap);
+    L.c2 = std::min<int64_t>(cap, 1LL << V2_MAX_LOG);
+    L.nb2_cap = 1LL << v2_bits(L.c2);
+    size_t o = 0;
+    L.hist = o;   o += 4 * (size_t)L.nbk_cap;
+    L.offs = o;   o += 4 * (size_t)(L.nbk_cap + 1);
+    L.cursor = o; o += 4 * (size_t)L.nbk_cap;
+    L.flags = o;  o += 4 * (size_t)(L.nbk_cap / SCAN_TILE + 2);
+    o = up256(o);
+    L.ctl = o;    o += 4 * 64;
+    L.cnt = o;    o += 4 * (size_t)L.nb2_cap;
+    L.boff = o;   o += 4 * (size_t)(L.nb2_cap + 1);
+    o = up256(o);
+    L.head = o;
+    L.pairs = o;  o = up256(o + 8 * (size_t)cap);
+    L.region = o; o = up256(o + 8 * (size_t)(L.nb2_cap * BCAP));
+    L.ovf = o;    o = up256(o + 8 * (size_t)L.c2);
+    L.ovf_b = o;  o = up256(o + 4 * (size_t)L.c2);
+    L.total = o;
+    return L;
 }
+}  // namespace
+
+size_t perm_scratch_bytes(int64_t n) { return layout(n).total; }
+size_t perm_scratch_head_bytes(int64_t n) { return layout(n).head; }
 
 PermScratch carve_perm_scratch(void *base, int64_t capacity, int64_t n) {
-    // Region offsets depend only on `capacity` so the zeroed histogram stays
-    // in place across calls with different n (the scan re-zeroes what it used).
+    const Layout L = layout(capacity);
+    char *c = (char *)base;
     PermScratch p;
     p.nb = bucket_bits(n);
     p.nbk = 1LL << p.nb;
-    const int64_t nbk_cap = 1LL << bucket_bits(capacity);
-    char *c = (char *)base;
-    c += sizeof(uint64_t) * (size_t)(capacity > 0 ? capacity : 1);
-    c = (char *)(((uintptr_t)c + 255) & ~(uintptr_t)255);
-    p.pairs = (uint64_t *)base;
-    p.hist = (uint32_t *)c;
-    p.offs = p.hist + nbk_cap;
-    p.cursor = p.offs + nbk_cap + 1;
-    p.flags = p.cursor + nbk_cap;     // tile sums (nbk_cap / SCAN_TILE + 1)
-    c = (char *)(p.flags + nbk_cap / SCAN_TILE + 2);
-    c = (char *)(((uintptr_t)c + 255) & ~(uintptr_t)255);
-    p.ticket = (uint32_t *)c;         // zero between uses (the last scan CTA resets it)
+    p.hist = (uint32_t *)(c + L.hist);
+    p.offs = (uint32_t *)(c + L.offs);
+    p.cursor = (uint32_t *)(c + L.cursor);
+    p.flags = (uint32_t *)(c + L.flags);
+    p.ctl = (uint32_t *)(c + L.ctl);
+    p.cnt = (uint32_t *)(c + L.cnt);
+    p.boff = (uint32_t *)(c + L.boff);
+    p.pairs = (uint64_t *)(c + L.pairs);
+    p.region = (uint64_t *)(c + L.region);
+    p.ovf = (uint64_t *)(c + L.ovf);
+    p.ovf_b = (uint32_t *)(c + L.ovf_b);
     p.v2 = n <= (1LL << V2_MAX_LOG) && capacity > 0;
     p.nb2 = v2_bits(n);
-    const int64_t c2 = std::min<int64_t>(capacity > 0 ? capacity : 1, 1LL << V2_MAX_LOG);
-    const int64_t nb2_cap = 1LL << v2_bits(c2);
-    p.tot = p.ticket + 64;
-    p.boff = p.tot + nb2_cap;
-    p.counts = p.boff + nb2_cap + 1;
-    const int64_t nblk_cap = (c2 + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
-    c = (char *)(p.counts + nblk_cap * nb2_cap);
-    p.tstate = (uint64_t *)(((uintptr_t)c + 255) & ~(uintptr_t)255);
     return p;
 }
 
@@ -650,18 +641,13 @@ static int perm_from_source(const Src &src, const SolveState *st, int64_t n, int
     if (n <= 0) return GLM_OK;
     if (!keys_array && sc.v2) {
         const int NB = 1 << sc.nb2;
-        const int nblk = key_blocks(n);
-        const size_t hsm = sizeof(uint32_t) * (size_t)NB;
         count_launch();
-        hist2_kernel<<<nblk, PERM_THREADS, hsm, stream>>>(src, n, sc.nb2, sc.counts, sc.tstate);
+        region_scatter_kernel<<<key_blocks(n), PERM_THREADS, sizeof(uint32_t) * (size_t)NB,
+                                stream>>>(src, n, sc.nb2, sc.cnt, sc.boff, sc.ctl, sc.region,
+                                          sc.ovf, sc.ovf_b);
         count_launch();
-        colscan2_kernel<<<(NB + 31) / 32, CS_WARPS * 32, 0, stream>>>(
-            st, sc.counts, nblk, sc.nb2, sc.tot, sc.boff, sc.ticket);
-        count_launch();
-        scatter2_kernel<<<nblk, PERM_THREADS, hsm, stream>>>(src, n, sc.nb2, sc.counts, sc.boff,
-                                                            sc.tstate, sc.pairs);
-        count_launch();
-        bsort2_kernel<<<NB, BS2_THREADS, 0, stream>>>(st, sc.pairs, sc.boff, sc.nb2, perm);
+        region_sort_kernel<<<NB, BS2_THREADS, 0, stream>>>(st, sc.region, sc.boff, sc.nb2, sc.ctl,
+                                                           sc.ovf, sc.ovf_b, sc.pairs, perm);
         GLM_CUDA_TRY(cudaGetLastError());
         return GLM_OK;
     }

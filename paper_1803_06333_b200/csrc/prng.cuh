@@ -13,18 +13,24 @@ struct PermScratch {
     uint32_t *hist = nullptr;    // zero between uses (scan re-zeroes it)
     uint32_t *offs = nullptr;    // nbk + 1
     uint32_t *cursor = nullptr;
-    uint32_t *flags = nullptr;   // [0] max bucket size
-    // row-count variant (generated keys, n <= 2^21)
+    uint32_t *flags = nullptr;   // tile sums
+    // bucket-region variant (generated keys, n <= 2^21)
     bool v2 = false;
     int nb2 = 0;
-    uint32_t *ticket = nullptr, *tot = nullptr, *boff = nullptr, *counts = nullptr;
-    uint64_t *tstate = nullptr;  // per-thread key-stream start states (pass 1 -> pass 2)
+    uint32_t *ctl = nullptr;     // [0] ticket, [1] overflow count (zero between uses), [2] total
+    uint32_t *cnt = nullptr;     // per-bucket totals (zero between uses)
+    uint32_t *boff = nullptr;    // bucket output offsets (nb2 buckets + 1)
+    uint64_t *region = nullptr;  // 1024 pairs per bucket
+    uint64_t *ovf = nullptr;     // pairs beyond their region, and their buckets
+    uint32_t *ovf_b = nullptr;
 };
 
 uint64_t host_jump(uint64_t state, uint64_t steps);
 int ensure_device_tables();
 int bucket_bits(int64_t n);
 size_t perm_scratch_bytes(int64_t n);
+// leading bytes holding the counters that must be zero before the first use
+size_t perm_scratch_head_bytes(int64_t n);
 // hist region must be zeroed once; bucket count follows n <= capacity
 PermScratch carve_perm_scratch(void *base, int64_t capacity, int64_t n);
 // Permutation of attempt `offset/n` of the stream whose start state is

@@ -1760,8 +1760,12 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     // permutation can be generated on the side stream into the other buffer
     // while this solve's epoch runs (overlapping value / finalize / the round
     // start instead of sitting between them and the next epoch).
+    static const int fork_mode = [] {        // experiments: 0 before / 1 after the epoch, 2 off
+        const char *e = getenv("GLM_PERM_FORK");
+        return e ? e[0] - '0' : 0;
+    }();
     const bool early = (a->flags & GLM_FLAG_PREFETCH_PERM) && s->host_known &&
-                       a->max_attempts == 1 && a->epochs == 1 && m > 0;
+                       a->max_attempts == 1 && a->epochs == 1 && m > 0 && fork_mode != 2;
     // GLM_FLAG_TURN: one attempt, and glm_round_turn follows on this stream
     const bool turn = (a->flags & GLM_FLAG_TURN) && a->max_attempts == 1 && a->epochs == 1 &&
                       m > 0;
@@ -1796,7 +1800,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
             s->prefetch_alt = true;
             return GLM_OK;
         };
-        if (early && launched == 0 && (r = fork())) return r;
+        if (early && launched == 0 && fork_mode == 0 && (r = fork())) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[1], stream));
         if (launched > 0) {   // attempt 0's snapshot was written by begin_kernel
             count_launch();
@@ -1813,6 +1817,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
                       : launch_async<false>(ep, lanes, a->max_inflight, a->flags, stream);
         }
         if (r) return r;
+        if (early && launched == 0 && fork_mode == 1 && (r = fork())) return r;
         if (s->timing) GLM_CUDA_TRY(event_record(ev[2], stream));
         if (!turn) {          // GLM_FLAG_TURN: glm_round_turn takes the value
             count_launch();
@@ -1897,7 +1902,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
         s->host_gen = next_state;
     } else {
         s->host_known = false;
-        if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0) {
+        if ((a->flags & GLM_FLAG_PREFETCH_PERM) && m > 0 && fork_mode != 2) {
             // generate the next solve's attempt-0 permutation from gen_next while
             // the caller runs its fold / all-reduce / round-start kernels
             if ((rc = ensure_side())) return rc;

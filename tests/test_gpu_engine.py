@@ -113,15 +113,19 @@ def _c2_like(n, d, k, seed):
                                 (vals * y[:, None]).reshape(-1), labels=y, validate=False)
 
 
-def test_async_engine_reaches_gap_target():
+@pytest.mark.parametrize("cache_flags", [0, 1, 2, 3])
+def test_async_engine_reaches_gap_target(cache_flags):
     """North-star async contract: async TPA-SCD reaches the deterministic
     (sequential) run's duality-gap target within +-10% of its epochs, on an
-    instance with the C2 shape ratios (40 nnz/example, d = n/10)."""
+    instance with the C2 shape ratios (40 nnz/example, d = n/10) — under every
+    cache policy (each its own scd_async instantiation over the packed
+    coordinate records: 1 = bench.py's C2, 3 = the C4 setting)."""
     m = _c2_like(200_000, 20_000, 40, 5)
     spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
     rounds = {}
     for mode in ("sequential", "async"):
-        eng = g.Engine(m, spec, g.HierarchyConfig(t1=80, seed=3, epochs=1), mode=mode)
+        eng = g.Engine(m, spec, g.HierarchyConfig(t1=80, seed=3, epochs=1), mode=mode,
+                       cache_flags=cache_flags)
         obj0, _ = eng.objective_and_gap()
         res = eng.train(g.StoppingCriteria(max_rounds=80, target_gap=1e-6 * abs(obj0)))
         assert res.stop_reason == "target_met", (mode, res.trace.rows[-1])
