@@ -447,9 +447,20 @@ __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
     const uint64_t s = q0 < n ? thread_apply(s_base) : 0ULL;
     walk_keys(s, n, [&](int64_t, uint32_t k) { atomicAdd(h3 + bucket_of(k, nb), 1u); });
     __syncthreads();
-    for (int i = threadIdx.x; i < NB; i += PERM_THREADS) {   // reserve this block's runs
-        const uint32_t c = h3[i];
-        h3[i] = c ? atomicAdd(cnt + i, c) : 0u;
+    {   // reserve this block's runs: every atomic in flight before any result is used
+        constexpr int PER = (1 << 12) / PERM_THREADS;
+        uint32_t r[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * PERM_THREADS;
+            const uint32_t c = i < NB ? h3[i] : 0u;
+            r[j] = c ? atomicAdd(cnt + i, c) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * PERM_THREADS;
+            if (i < NB) h3[i] = r[j];
+        }
     }
     __syncthreads();
     walk_keys(s, n, [&](int64_t q, uint32_t k) {
@@ -464,9 +475,14 @@ __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
             ovf_b[o] = b;
         }
     });
-    __threadfence();
+    // the last CTA needs only the totals: their atomics returned before the
+    // barrier, thread 0's fence orders them before the ticket (the region
+    // pairs are for the next kernel, ordered by the kernel boundary)
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(ctl, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ctl, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (s_last) {       // every block's reservations are in: bucket output offsets
         __threadfence();
