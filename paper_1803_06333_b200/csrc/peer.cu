@@ -810,9 +810,13 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
         if (e != cudaSuccess) return glm_set_cuda_error(e, "glm_peer_create", __FILE__, __LINE__);
         return glm_set_error(GLM_USAGE, "round_turn_kernel cannot be resident on this device");
     }
-    int per_sm = occ < 2 ? occ : 2;
+    // one block per SM: the rest of the SM takes the permutation prefetch and
+    // the next epoch's first CTAs while the turn waits on its peers (bench.py
+    // C2, one box, 3 runs each: 2 per SM -> 1 per SM 3713 -> 3829 epochs/s at 2
+    // ranks, 6347 -> 6769 at 4; at 1 rank with the early release 1934)
+    int per_sm = 1;
     if (const char *env = getenv("GLM_TURN_BLOCKS_PER_SM"))   // experiments: 1 or 2
-        per_sm = atoi(env) >= 1 && atoi(env) <= per_sm ? atoi(env) : per_sm;
+        per_sm = atoi(env) >= 1 && atoi(env) <= (occ < 2 ? occ : 2) ? atoi(env) : per_sm;
     p->turn_blocks = per_sm * sms;
     if (p->turn_blocks > PEER_BLOCKS) p->turn_blocks = PEER_BLOCKS;
     p->ctl = reinterpret_cast<int64_t *>(p->mem);
@@ -968,6 +972,10 @@ int glm_round_turn(glm_peer *p, glm_solver *s, int kind, double lam, double quad
         return glm_set_error(GLM_USAGE, "null argument to glm_round_turn");
     if (p->d != d || d > s->max_rows || m > s->max_coords)
         return glm_set_error(GLM_USAGE, "glm_round_turn sizes do not match");
+    // measured (bench.py C2, one box, 3 runs each): at 1 rank the epoch's
+    // early release of this kernel pays (1906 -> 1934 epochs/s); with peers
+    // it costs (3829 -> 3749 at 2 ranks, 6769 -> 6697 at 4)
+    s->early_trigger = p->world == 1 ? 1 : 0;
     TurnParams a{};
     a.st = s->st;
     a.view0 = s->view[0];

@@ -117,10 +117,23 @@ __device__ __forceinline__ void store_block_gsum(double g, double *gpart, SolveS
 // (the kernel then reads indptr).
 constexpr int64_t META_CNT_SENTINEL = (1LL << 24) - 1;
 
+// GLM_EPOCH_EARLY_TRIGGER=0|1 (experiments) overrides glm_solver::early_trigger
+static int epoch_early_trigger(const glm_solver *s) {
+    static const int v = [] {
+        const char *e = getenv("GLM_EPOCH_EARLY_TRIGGER");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return v >= 0 ? v : (s->early_trigger ? 1 : 0);
+}
+
 template <int G, int R, bool DENSE, int CM>
 __global__ void __launch_bounds__(256) scd_async(EpochParams p) {
     SolveState *st = p.st;
     pdl_wait();
+    // pdl 2: the round turn may be scheduled at once — its blocks take SM
+    // slots as this grid's CTAs retire (one full wave, so none is displaced)
+    // and wait in griddepcontrol.wait for this grid to complete
+    if (p.pdl == 2) pdl_trigger();
     if (skip_attempt(st, p.seq)) return;
     tl_start(TL_EPOCH);
     // CM bit 0: gather the view through L1 (ld.ca); bit 1: stream the column
@@ -1769,7 +1782,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     // GLM_FLAG_TURN: one attempt, and glm_round_turn follows on this stream
     const bool turn = (a->flags & GLM_FLAG_TURN) && a->max_attempts == 1 && a->epochs == 1 &&
                       m > 0;
-    ep.pdl = turn ? 1 : 0;        // the epoch follows the previous round's turn kernel
+    ep.pdl = turn ? 1 + epoch_early_trigger(s) : 0;   // follows the previous round's turn
     const uint64_t next_state = early ? host_jump(s->host_gen, (uint64_t)m) : 0;
     auto ensure_side = [&]() -> int { return ensure_side_stream(s); };
     int launched = 0;

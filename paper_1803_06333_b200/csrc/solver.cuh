@@ -9,6 +9,9 @@
 
 struct glm_solver {
     int device = 0;
+    // the async epoch after a round turn releases the next turn at its start
+    // (set by glm_round_turn: 1 rank) instead of at its end
+    int early_trigger = 0;
     int64_t max_coords = 0, max_rows = 0;
     glm::SolveState *st = nullptr;        // device
     glm::SolveState *st_host = nullptr;   // pinned mirror
