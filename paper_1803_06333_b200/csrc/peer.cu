@@ -810,11 +810,14 @@ int glm_peer_create(int device, int64_t d, int rank, int world, glm_peer **out) 
         if (e != cudaSuccess) return glm_set_cuda_error(e, "glm_peer_create", __FILE__, __LINE__);
         return glm_set_error(GLM_USAGE, "round_turn_kernel cannot be resident on this device");
     }
-    // one block per SM: the rest of the SM takes the permutation prefetch and
-    // the next epoch's first CTAs while the turn waits on its peers (bench.py
-    // C2, one box, 3 runs each: 2 per SM -> 1 per SM 3713 -> 3829 epochs/s at 2
-    // ranks, 6347 -> 6769 at 4; at 1 rank with the early release 1934)
-    int per_sm = 1;
+    // A short Delta v (C2: 100k rows) leaves the turn latency-bound: one block
+    // per SM, and the rest of the SM takes the permutation prefetch and the
+    // next epoch's first CTAs while the turn waits on its peers (bench.py C2,
+    // one box, 3 runs each: 2 per SM -> 1 per SM 3713 -> 3829 epochs/s at 2
+    // ranks, 6347 -> 6769 at 4; at 1 rank with the early release 1934).  A long
+    // one (C4: 10M rows) makes P1 and P3 bandwidth passes that want every
+    // thread: 2 per SM (1 per SM: 330 -> 297 epochs/s at 2 ranks, 495 -> 457 at 4).
+    int per_sm = d >= (int64_t)1 << 20 ? (occ < 2 ? occ : 2) : 1;
     if (const char *env = getenv("GLM_TURN_BLOCKS_PER_SM"))   // experiments: 1 or 2
         per_sm = atoi(env) >= 1 && atoi(env) <= (occ < 2 ? occ : 2) ? atoi(env) : per_sm;
     p->turn_blocks = per_sm * sms;
