@@ -37,6 +37,7 @@
 // jumps (one warp matrix-vector product instead of a chain of ~20 dependent
 // jump-table loads); the attempt offset, when not 0, is one warp_jump.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -428,8 +429,8 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_
 // cnt: per-bucket totals.  Both are zero between uses (the last CTA resets).
 template <class Src>
 __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
-    Src src, int64_t n, int nb, uint32_t *cnt, uint32_t *boff, uint32_t *ctl, uint64_t *region,
-    uint64_t *ovf, uint32_t *ovf_b) {
+    Src src, int64_t n, int nb, uint32_t cap, uint32_t *cnt, uint32_t *boff, uint32_t *ctl,
+    uint64_t *region, uint64_t *ovf, uint32_t *ovf_b) {
     if (src.skip()) return;
     tl_start(TL_PERM_FIRST);
     extern __shared__ uint32_t h3[];
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
         const uint32_t b = bucket_of(k, nb);
         const uint32_t pos = atomicAdd(h3 + b, 1u);
         const uint64_t pr = ((uint64_t)k << 32) | (uint32_t)q;
-        if (pos < (uint32_t)BCAP) {
+        if (pos < cap) {
             region[(size_t)b * BCAP + pos] = pr;
         } else {
             const uint32_t o = atomicAdd(ctl + 1, 1u);
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
 // insertion-sorts sub-bucket t by (key, index) — numpy's stable order — and
 // the CTA writes its slice of the permutation coalesced.
 __global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
-    const SolveState *st, const uint64_t *region, const uint32_t *boff, int nb,
+    const SolveState *st, const uint64_t *region, const uint32_t *boff, int nb, int cap,
     const uint32_t *ctl, const uint64_t *ovf, const uint32_t *ovf_b, uint64_t *tmp,
     int32_t *perm) {
     if (st && st->done) return;
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
     const int cnt = (int)(hi - lo);
     const uint64_t *src = region + (size_t)blockIdx.x * BCAP;
     const int t = threadIdx.x;
-    if (cnt <= BCAP) {
+    if (cnt <= cap) {
         const int sh = 24 - nb;                    // the 8 key bits below the bucket bits
         s_cur[t] = 0;
         __syncthreads();
@@ -552,9 +553,9 @@ __global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
         __syncthreads();
         for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)s_out[i];
     } else {            // the bucket outgrew its region: region + overflow list, slowly
-        for (int i = t; i < BCAP; i += BS2_THREADS) tmp[lo + i] = src[i];
+        for (int i = t; i < cap; i += BS2_THREADS) tmp[lo + i] = src[i];
         if (t == 0) {
-            int w = BCAP;
+            int w = cap;
             const uint32_t no = ctl[2];
             for (uint32_t o = 0; o < no; ++o)
                 if (ovf_b[o] == blockIdx.x) tmp[lo + w++] = ovf[o];
@@ -565,6 +566,17 @@ __global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
         for (int i = t; i < cnt; i += BS2_THREADS) perm[lo + i] = (int32_t)(uint32_t)tmp[lo + i];
     }
     tl_end(TL_PERM_LAST);
+}
+
+// Usable pairs per bucket region: BCAP; GLM_PERM_REGION_CAP (tests) lowers it
+// so that buckets overflow and the slow path runs.
+static int region_cap() {
+    static const int v = [] {
+        const char *e = getenv("GLM_PERM_REGION_CAP");
+        const int c = e ? atoi(e) : BCAP;
+        return c >= 1 && c <= BCAP ? c : BCAP;
+    }();
+    return v;
 }
 
 static int v2_bits(int64_t n) {       // <= 512 keys per bucket on average, <= 4096 buckets
@@ -659,11 +671,12 @@ static int perm_from_source(const Src &src, const SolveState *st, int64_t n, int
         const int NB = 1 << sc.nb2;
         count_launch();
         region_scatter_kernel<<<key_blocks(n), PERM_THREADS, sizeof(uint32_t) * (size_t)NB,
-                                stream>>>(src, n, sc.nb2, sc.cnt, sc.boff, sc.ctl, sc.region,
-                                          sc.ovf, sc.ovf_b);
+                                stream>>>(src, n, sc.nb2, (uint32_t)region_cap(), sc.cnt, sc.boff,
+                                          sc.ctl, sc.region, sc.ovf, sc.ovf_b);
         count_launch();
-        region_sort_kernel<<<NB, BS2_THREADS, 0, stream>>>(st, sc.region, sc.boff, sc.nb2, sc.ctl,
-                                                           sc.ovf, sc.ovf_b, sc.pairs, perm);
+        region_sort_kernel<<<NB, BS2_THREADS, 0, stream>>>(st, sc.region, sc.boff, sc.nb2,
+                                                           region_cap(), sc.ctl, sc.ovf, sc.ovf_b,
+                                                           sc.pairs, perm);
         GLM_CUDA_TRY(cudaGetLastError());
         return GLM_OK;
     }

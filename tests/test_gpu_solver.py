@@ -57,6 +57,21 @@ def test_permutation_large_vs_oracle():
         assert gen.state == st
 
 
+@pytest.mark.parametrize("cap", ["1", "96"])
+def test_permutation_region_overflow_path(cap):
+    """Bucket regions shrunk to `cap` pairs (GLM_PERM_REGION_CAP, read once per
+    process, hence the subprocess): the spill lists and the slow sort path give
+    the same permutations as the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "perm_overflow_check.py")],
+                       env=dict(os.environ, GLM_PERM_REGION_CAP=cap), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "overflow path ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_chunk_keys_bit_exact(golden):
     z = golden("prng")
     from paper_1803_06333_b200 import pipeline
