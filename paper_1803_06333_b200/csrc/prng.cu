@@ -428,7 +428,14 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_
 // Pass 1.  ctl: [0] ticket, [1] overflow count, [2] overflow total (for pass 2);
 // cnt: per-bucket totals.  Both are zero between uses (the last CTA resets).
 template <class Src>
-__global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
+// <= 48 registers (5 CTAs per SM worth): a CTA fits beside the two CTAs of
+// the epoch kernel (scd.cu, 104 registers), so the next round's permutation
+// runs under the epoch (GLM_PERM_LEAN overrides for experiments)
+#ifndef GLM_PERM_LEAN
+#define GLM_PERM_LEAN 5
+#endif
+#define PERM_BOUNDS __launch_bounds__(PERM_THREADS, GLM_PERM_LEAN)
+__global__ void PERM_BOUNDS region_scatter_kernel(
     Src src, int64_t n, int nb, uint32_t cap, uint32_t *cnt, uint32_t *boff, uint32_t *ctl,
     uint64_t *region, uint64_t *ovf, uint32_t *ovf_b) {
     if (src.skip()) return;
@@ -517,7 +524,7 @@ __global__ void __launch_bounds__(PERM_THREADS) region_scatter_kernel(
 // the pairs over 256 sub-buckets in shared memory (~2 pairs each), thread t
 // insertion-sorts sub-bucket t by (key, index) — numpy's stable order — and
 // the CTA writes its slice of the permutation coalesced.
-__global__ void __launch_bounds__(BS2_THREADS) region_sort_kernel(
+__global__ void PERM_BOUNDS region_sort_kernel(
     const SolveState *st, const uint64_t *region, const uint32_t *boff, int nb, int cap,
     const uint32_t *ctl, const uint64_t *ovf, const uint32_t *ovf_b, uint64_t *tmp,
     int32_t *perm) {

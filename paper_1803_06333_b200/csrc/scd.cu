@@ -126,8 +126,19 @@ static int epoch_early_trigger(const glm_solver *s) {
     return v >= 0 ? v : (s->early_trigger ? 1 : 0);
 }
 
+// 104 registers (2 CTAs of 256 threads: 53 K of the SM's 64 K) leave room for
+// one 256-thread CTA of <= 48 registers next to the epoch on every SM — the
+// side-stream permutation of the next round (prng.cu region kernels) then runs
+// under the epoch instead of taking SM slots from the next turn and epoch.
+// Measured (bench.py C2, one 4-GPU box, 2 runs each; 121 registers before):
+// 1924 -> 1994 / 3816 -> 3947 / 6760 -> 7003 epochs/s at 1 / 2 / 4 GPUs, C4
+// 194 -> 198.  No spills in the sparse instantiations (GLM_EPOCH_MAXNREG
+// overrides for experiments).
+#ifndef GLM_EPOCH_MAXNREG
+#define GLM_EPOCH_MAXNREG 104
+#endif
 template <int G, int R, bool DENSE, int CM>
-__global__ void __launch_bounds__(256) scd_async(EpochParams p) {
+__global__ void __maxnreg__(GLM_EPOCH_MAXNREG) scd_async(EpochParams p) {
     SolveState *st = p.st;
     pdl_wait();
     // pdl 2: the round turn may be scheduled at once — its blocks take SM
