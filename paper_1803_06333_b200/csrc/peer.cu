@@ -465,6 +465,7 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
 }
 
 constexpr int TURN_THREADS = 512;
+constexpr int TURN_UNROLL = 2;      // rows per thread and pass in P1 / P3
 
 __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) {
     __shared__ double sm[32 * 4];      // block_sum<4>
@@ -500,21 +501,38 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         const double *V = vw0 ? p.view1 : p.view0;
         const bool dual = kind_is_dual(p.kind);
         double acc[3] = {0.0, 0.0, 0.0};           // f(v), view terms, non-finite
-        for (int64_t r = tid; r < p.d; r += nth) {
-            const double x = __ldcg(V + r), l = p.lin[r], vr = p.v[r];
-            const double u = x - l;
-            out[r] = u / p.quad;
-            double f, g;                            // outer_model_kernel's arithmetic
-            if (dual) {
-                f = vr * vr;
-            } else {
-                f_terms(p.kind, p.lam, p.tgt[r], vr, f, g);
-                if (f_halved(p.kind)) f *= 2.0;
+        // TURN_UNROLL rows per thread and pass, every load issued before any
+        // is used (the same rows per thread and the same summation order as a
+        // plain grid-stride loop)
+        for (int64_t r0 = tid; r0 < p.d; r0 += TURN_UNROLL * nth) {
+            double x[TURN_UNROLL], l[TURN_UNROLL], vr[TURN_UNROLL], t[TURN_UNROLL];
+#pragma unroll
+            for (int k = 0; k < TURN_UNROLL; ++k) {
+                const int64_t r = r0 + k * nth;
+                const bool in = r < p.d;
+                x[k] = in ? __ldcg(V + r) : 0.0;
+                l[k] = in ? p.lin[r] : 0.0;
+                vr[k] = in ? p.v[r] : 0.0;
+                t[k] = in && !dual ? p.tgt[r] : 0.0;
             }
-            acc[0] += f;
-            if (active) {
-                if (!isfinite(x)) acc[2] += 1.0;
-                acc[1] += l * u + 0.5 * u * u;
+#pragma unroll
+            for (int k = 0; k < TURN_UNROLL; ++k) {
+                const int64_t r = r0 + k * nth;
+                if (r >= p.d) break;
+                const double u = x[k] - l[k];
+                out[r] = u / p.quad;
+                double f, g;                        // outer_model_kernel's arithmetic
+                if (dual) {
+                    f = vr[k] * vr[k];
+                } else {
+                    f_terms(p.kind, p.lam, t[k], vr[k], f, g);
+                    if (f_halved(p.kind)) f *= 2.0;
+                }
+                acc[0] += f;
+                if (active) {
+                    if (!isfinite(x[k])) acc[2] += 1.0;
+                    acc[1] += l[k] * u + 0.5 * u * u;
+                }
             }
         }
         block_sum<3>(acc, sm);
@@ -622,28 +640,79 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
     const int64_t R = s_R + 1;
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
-            // one poller per rank watches the local flag slots (the peers
-            // store into them over NVLink), then releases a local "every rank
-            // published R" word (ctl[3]) and their accept bits (ctl[4]) for the
-            // other blocks
+            // block 0 waits with the deadline and relays what it saw (ctl[3],
+            // the accept bits in ctl[4]) for a rank that missed it
             const uint32_t mask = wait_flags(p.flags_in, p.world, R, p.ctl, p.timeout);
             s_acc = mask;
             p.ctl[4] = (int64_t)mask;
             __threadfence();
             atomicMax(reinterpret_cast<unsigned long long *>(p.ctl + 3), (unsigned long long)R);
         } else {
+            // the other blocks read the local flag slots themselves (the peers
+            // store into them over NVLink) — one hop less than block 0's relay
             uint64_t t0 = 0;
-            while ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) < R) {
+            for (;;) {
+                uint32_t mask = 0;
+                bool all = true;
+                for (int j = 0; j < p.world && all; ++j) {
+                    const int64_t f = ld_acquire_sys(p.flags_in + j);
+                    if ((f >> 2) < R) all = false;
+                    else mask |= (uint32_t)((f >> (R & 1)) & 1) << j;
+                }
+                if (all) {
+                    s_acc = mask;
+                    break;
+                }
+                if ((int64_t)ld_acquire_gpu_u64(p.ctl + 3) >= R) {
+                    s_acc = (uint32_t)*(volatile int64_t *)(p.ctl + 4);
+                    break;
+                }
                 __nanosleep(32);
                 if (expired(t0, 2 * p.timeout)) {    // block 0's own wait has the deadline
                     peer_fail(p.ctl, PEER_ERR_GRID, 3);
+                    s_acc = 0;
                     break;
                 }
             }
-            s_acc = (uint32_t)*(volatile int64_t *)(p.ctl + 4);
         }
     }
-    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[3] = gtimer();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (p.stamps) p.stamps[3] = gtimer();
+        // every block read the decision right after the P1 -> P2 barrier (long
+        // done): block 0 resets the solver state for the next round here, off
+        // the kernel's tail.  f(v), the constant and G(0) of the next round are
+        // formed by its P1.
+        uint64_t t0 = 0;
+        while (ld_acquire_gpu_u32(&st->block_counter) < gridDim.x) {
+            __nanosleep(32);
+            if (expired(t0, p.timeout)) {
+                peer_fail(p.ctl, PEER_ERR_GRID, 4);
+                break;
+            }
+        }
+        st->block_counter = 0;
+        p.ctl[1] = R;
+        if (st->status == GLM_OK) {                 // else keep the error visible to the host
+            st->gen_state = st->gen_next;           // begin_kernel with reuse_gsum
+            // damping: an accepted (or plateaued) attempt resets it like the
+            // reference's per-round reset (engine.py:251-252); a rejected one
+            // keeps the halved value, so the next round is the retry
+            // damped_solve would have made (solver.py:282-293) and consecutive
+            // rejections reach the floor and GLM_DIVERGENCE (decide_cached)
+            // instead of looping at damping 1
+            if (st->epochs_run > 0 || st->plateaued) st->damping = 1.0;
+            st->epochs_target = p.epochs;
+            st->epochs_run = 0;
+            st->retries = 0;
+            st->plateaued = 0;
+            st->attempts = 0;
+            st->status = GLM_OK;
+            st->done = 0;
+            st->dc = -1;
+            st->vw = 0;
+            st->epoch_blocks = 0;
+        }
+    }
     __syncthreads();
     const int64_t off = (R & 1) * p.pstride;
     const uint32_t accm = s_acc;
@@ -684,54 +753,39 @@ __global__ void __launch_bounds__(TURN_THREADS) round_turn_kernel(TurnParams p) 
         }
         __syncthreads();
     }
-    for (int64_t r = tid; r < p.d; r += nth) {
-        const double s = p.rs ? __ldcg(p.red[r / cs] + off + r) : rank_sum(p.bufs, p.world, off + r, accm);
-        const double x = p.v[r] + s;
-        p.v[r] = x;
-        double f, g;
-        if (dual) {
-            g = x / p.lam;
-        } else {
-            f_terms(p.kind, p.lam, p.tgt[r], x, f, g);
+    for (int64_t r0 = tid; r0 < p.d; r0 += TURN_UNROLL * nth) {
+        double sm2[TURN_UNROLL], v0[TURN_UNROLL];
+#pragma unroll
+        for (int k = 0; k < TURN_UNROLL; ++k) {   // every rank's rows in flight together
+            const int64_t r = r0 + k * nth;
+            const bool in = r < p.d;
+            sm2[k] = !in ? 0.0
+                         : p.rs ? __ldcg(p.red[r / cs] + off + r)
+                                : rank_sum(p.bufs, p.world, off + r, accm);
+            v0[k] = in ? p.v[r] : 0.0;
         }
-        p.grad[r] = g;
-        p.lin[r] = g;
-        p.view0[r] = g;
-        p.view1[r] = g;
-    }
-    // f(v), the constant and G(0) of the next round are formed by its P1;
-    // block 0 resets the solver state once every block has read the decision
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    uint64_t t0 = 0;
-    while (ld_acquire_gpu_u32(&st->block_counter) < gridDim.x) {
-        __nanosleep(32);
-        if (expired(t0, p.timeout)) {
-            peer_fail(p.ctl, PEER_ERR_GRID, 4);
-            break;
+#pragma unroll
+        for (int k = 0; k < TURN_UNROLL; ++k) {
+            const int64_t r = r0 + k * nth;
+            if (r >= p.d) break;
+            const double x = v0[k] + sm2[k];
+            p.v[r] = x;
+            double f, g;
+            if (dual) {
+                g = x / p.lam;
+            } else {
+                f_terms(p.kind, p.lam, p.tgt[r], x, f, g);
+            }
+            p.grad[r] = g;
+            p.lin[r] = g;
+            p.view0[r] = g;
+            p.view1[r] = g;
         }
     }
-    st->block_counter = 0;
-    tl_end(TL_TURN);
-    p.ctl[1] = R;
-    if (p.stamps) p.stamps[4] = gtimer();
-    if (st->status != GLM_OK) return;          // keep a solver error visible to the host
-    st->gen_state = st->gen_next;              // begin_kernel with reuse_gsum
-    // damping: an accepted (or plateaued) attempt resets it like the
-    // reference's per-round reset (engine.py:251-252); a rejected one keeps
-    // the halved value, so the next round is the retry damped_solve would have
-    // made (solver.py:282-293) and consecutive rejections reach the floor and
-    // GLM_DIVERGENCE (decide_cached) instead of looping at damping 1
-    if (st->epochs_run > 0 || st->plateaued) st->damping = 1.0;
-    st->epochs_target = p.epochs;
-    st->epochs_run = 0;
-    st->retries = 0;
-    st->plateaued = 0;
-    st->attempts = 0;
-    st->status = GLM_OK;
-    st->done = 0;
-    st->dc = -1;
-    st->vw = 0;
-    st->epoch_blocks = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        tl_end(TL_TURN);
+        if (p.stamps) p.stamps[4] = gtimer();    // block 0's own P3 rows done
+    }
 }
 
 __global__ void peer_consume_kernel(int64_t *ctl) { ctl[1] = ctl[0]; }
