@@ -122,6 +122,8 @@ class NcclReducer:
         # may then share one GPU, which NCCL refuses)
         self.staged = not self.on_cuda
         self._aborted = False
+        self._hbuf = None          # reusable device buffer for host vectors (NCCL)
+        self._chk = None           # the length check's [n, -n], device + pinned host
 
     def handshake(self):
         probe = torch.tensor([self.rank, PROTOCOL_VERSION], dtype=torch.float64,
@@ -139,9 +141,45 @@ class NcclReducer:
             return vec.to(self.device, torch.float64).contiguous(), True
         return torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64)).to(self.device), False
 
+    def _allreduce_host(self, vec, out):
+        """A host vector through NCCL: one reusable device buffer, copies from
+        and to page-locked arrays asynchronous, the length check's collective
+        queued behind the upload (one host synchronisation before the data
+        collective, one after the download)."""
+        src = np.ascontiguousarray(vec, dtype=np.float64)
+        n = int(src.size)
+        if self._hbuf is None or self._hbuf.numel() != n:
+            self._hbuf = torch.empty(n, dtype=torch.float64, device=self.device)
+        buf = self._hbuf
+        h = torch.from_numpy(src)
+        buf.copy_(h, non_blocking=h.is_pinned())
+        if self.world > 1:          # max(n) == -max(-n), as allreduce_sum checks it
+            if self._chk is None:
+                self._chk = (torch.empty(2, dtype=torch.int64, device=self.device),
+                             torch.empty(2, dtype=torch.int64, pin_memory=True))
+            dchk, hchk = self._chk
+            hchk[0], hchk[1] = n, -n
+            dchk.copy_(hchk, non_blocking=True)
+            dist.all_reduce(dchk, op=dist.ReduceOp.MAX, group=self.group)
+            hi, neg_lo = dchk.tolist()
+            if hi != -neg_lo:
+                raise ProtocolError("vector length mismatch")
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+        dst = out if out is not None else np.empty(n, dtype=np.float64)
+        hd = torch.from_numpy(dst)
+        pinned = hd.is_pinned()
+        hd.copy_(buf, non_blocking=pinned)
+        if pinned:
+            torch.cuda.current_stream(self.device).synchronize()
+        return dst
+
     def allreduce_sum(self, vec, out=None):
         if self._aborted:
             raise ReduceError("collective aborted")
+        if (isinstance(vec, np.ndarray) and not self.deterministic and not self.staged
+                and (out is None or (isinstance(out, np.ndarray) and out.dtype == np.float64
+                                     and out.flags.c_contiguous))):
+            return self._allreduce_host(vec, out)
         t, was_tensor = self._tensor(vec)
         if self.world > 1:     # one collective checks the lengths: max(n) == -max(-n)
             n = torch.tensor([t.numel(), -t.numel()], dtype=torch.int64, device=self.device)

@@ -125,6 +125,21 @@ def main():
     m = matrix()
     if args.kill:
         return kill(rank, world, m)
+    if not args.same_gpu:      # NcclReducer's host-vector path (pinned and pageable)
+        red = NcclReducer()
+        for n in (100_003, 7):
+            vecs = [np.random.default_rng(100 + r).standard_normal(n) for r in range(world)]
+            want = vecs[0].copy()
+            for r in range(1, world):
+                want = want + vecs[r]
+            pin = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+            pin[:] = vecs[rank]
+            got = red.allreduce_sum(pin, out=pin)
+            assert got is pin and np.array_equal(pin, want), "pinned host allreduce"
+            got2 = red.allreduce_sum(vecs[rank].copy())
+            assert np.array_equal(got2, want), "pageable host allreduce"
+        if rank == 0:
+            print("HOST ALLREDUCE OK", flush=True)
     parity(rank, world, m, ("sequential", "sequential", "async"))
     sys.stdout.flush()
     shutdown()

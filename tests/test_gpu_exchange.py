@@ -112,6 +112,7 @@ def test_two_process_exchange_matches_nccl():
         pytest.skip("needs 2 GPUs")
     out = _torchrun()
     assert out.returncode == 0, _why(out)
+    assert "HOST ALLREDUCE OK" in out.stdout, out.stdout[-2000:]
     assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
     assert "GRAPH async OK" in out.stdout, out.stdout[-2000:]
 
