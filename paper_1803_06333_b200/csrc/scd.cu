@@ -1544,10 +1544,16 @@ static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
     return GLM_OK;
 }
 
-static int auto_lanes(double avg_nnz) {   // lanes x registers cover the column
+static int auto_lanes(double avg_nnz, bool dense, int64_t d) {   // lanes x registers cover the column
     if (avg_nnz <= 16) return 4;
     if (avg_nnz <= 40) return 4 | (10 << 8);   // C2 / C5: 4 lanes x 10 registers (tools/sweep_c2.py)
     if (avg_nnz <= 64) return 8;
+    // sparse columns of a few hundred rows into an L2-resident view: more
+    // coordinates in flight beat more lanes per coordinate (C2 primal, 400 nnz
+    // per feature into a 1M-row view: 32 lanes 0.63-0.67 ms, 16 x 4 0.55-0.56,
+    // 8 x 5 0.53 per epoch); a view beyond L2 wants 32 lanes (C4, 10M rows:
+    // 32 lanes 5.03 ms, 16 x 4 5.21; tools/gpu_c2p2.sh)
+    if (!dense && avg_nnz <= 1024 && d <= ((int64_t)1 << 22)) return 8 | (5 << 8);
     return 32;
 }
 
@@ -1724,7 +1730,7 @@ int solve(glm_solver *s, const glm_matrix *A, const glm_solve_args *a, double *d
     vp.seq = -1;
 
     const double avg = dense ? (double)d : (m > 0 ? (double)A->nnz / (double)m : 0.0);
-    const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg);
+    const int lanes = a->group_lanes > 0 ? a->group_lanes : auto_lanes(avg, dense, d);
     const int seq_bs = avg <= 96.0 ? 32 : 256;
     // the per-attempt value pass over the view: ~4 rows per thread keeps the
     // block partials (and the last block's fold) short
@@ -2139,7 +2145,7 @@ int chunk_enqueue(glm_solver *s, const StreamSolve &a, const ChunkJob &c, cudaSt
     vp.dfull = nullptr;
     const bool dense = A->layout == GLM_DENSE;
     const double avg = dense ? (double)d : (nc > 0 ? (double)A->nnz / (double)nc : 0.0);
-    const int lanes = a.group_lanes > 0 ? a.group_lanes : auto_lanes(avg);
+    const int lanes = a.group_lanes > 0 ? a.group_lanes : auto_lanes(avg, dense, d);
     for (int i = 0; i < c.attempts && nc > 0; ++i) {
         count_launch();
         snapshot_kernel<<<grid_stride_blocks(d), 256, 0, stream>>>(s->st, s->view[0], s->view[1],

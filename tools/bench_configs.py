@@ -156,7 +156,8 @@ def engine_modes(dm, spec, args, alg_bytes, n_coords, seq_rounds=None):
     out = {}
     for mode in ("async", "sequential"):
         rounds = args.rounds if mode == "async" else (seq_rounds or args.seq_rounds)
-        kw = dict(sync_solves=False, retry_budget=0, cache_flags=1) if mode == "async" else {}
+        kw = dict(sync_solves=False, retry_budget=0, cache_flags=1,
+                  group_lanes=getattr(args, "lanes", 0)) if mode == "async" else {}
         eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode=mode, **kw)
         r = timed_rounds(eng, rounds)
         ms = float(np.median(r["round_ms"][1:] if len(r["round_ms"]) > 2 else r["round_ms"]))
@@ -290,8 +291,9 @@ def c4(args):
     res = {"config": "C4", "workload": f"lasso (primal), sparse {n_ex}x{n_feat}, "
                                        f"{per_col} nnz/feature, lambda={lam}", "nnz": nnz}
     eng = g.Engine(dm, spec, g.HierarchyConfig(seed=0, epochs=1), mode="async",
-                   sync_solves=False, cache_flags=args.cache_flags)
+                   sync_solves=False, cache_flags=args.cache_flags, group_lanes=args.lanes)
     res["cache_flags"] = args.cache_flags
+    res["lanes"] = args.lanes
     ms_all = []
     objs = []
     for r in range(args.rounds):
@@ -410,6 +412,8 @@ def main():
     ap.add_argument("--n-feat", type=int, default=1_000_000)
     ap.add_argument("--per-col", type=int, default=400)
     ap.add_argument("--inflight", type=int, default=0, help="async in-flight budget (0 = auto)")
+    ap.add_argument("--lanes", type=int, default=0,
+                    help="async lanes per coordinate: G | (R << 8) (0 = auto)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     if args.config == "c3":
