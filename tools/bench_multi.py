@@ -138,6 +138,28 @@ def c4(args, rank, world):
         eng.outer_round()
     eng.reset()
     ms, objs = timed(eng, args.rounds, gap=False)
+    breakdown = None
+    if args.breakdown:      # per-kernel events of extra rounds + the turn's phase stamps
+        wk = next(iter(eng.workers.values()))
+        st = torch.zeros(8, dtype=torch.int64, device="cuda")
+        if eng.exchange is not None:
+            L.check(L.lib().glm_peer_stamps(eng.exchange.handle, st.data_ptr()), "stamps")
+        wk.solver.timing_read()
+        wk.solver.timing_glue()
+        wk.solver.timing(True)
+        for _ in range(3):
+            eng.outer_round()
+        torch.cuda.synchronize()
+        k_ms, k_n = wk.solver.timing_read()
+        gl_ms, gl_n = wk.solver.timing_glue()
+        wk.solver.timing(False)
+        s_ = st.cpu().numpy().astype(np.int64)
+        breakdown = {"perm_ms": k_ms[0] / max(k_n, 1), "epoch_ms": k_ms[1] / max(k_n, 1),
+                     "turn_ms": gl_ms[2] / max(gl_n[2], 1),
+                     "turn_phases_us": (np.diff(s_[:5]) / 1e3).round(2).tolist()
+                     if eng.exchange is not None else None}
+        if eng.exchange is not None:
+            L.lib().glm_peer_stamps(eng.exchange.handle, None)
     nnz = n_tot * per_col
     alg = 12 * nnz + 36 * n_tot
     med = float(np.median(ms[1:]))
@@ -149,7 +171,7 @@ def c4(args, rank, world):
             "hbm_frac_per_gpu": alg / world / (med * 1e-3) / 1e9 / HBM,
             "objective": objs, "round_ms": ms,
             "exchange": "nvlink-peer" if eng.exchange else "nccl",
-            "exchange_bytes_per_rank_per_round": 8 * n_ex}
+            "exchange_bytes_per_rank_per_round": 8 * n_ex, "breakdown": breakdown}
 
 
 def c5(args, rank, world):
@@ -247,6 +269,8 @@ def main():
     ap.add_argument("--n-feat", type=int, default=1_000_000)
     ap.add_argument("--per-col", type=int, default=400)
     ap.add_argument("--out", default=None, help="append the JSON line to this file")
+    ap.add_argument("--breakdown", action="store_true",
+                    help="C4: per-kernel times and the turn's phase stamps of 3 extra rounds")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
