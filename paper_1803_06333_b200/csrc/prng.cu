@@ -425,9 +425,6 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t *s_
     return pre;
 }
 
-// Pass 1.  ctl: [0] ticket, [1] overflow count, [2] overflow total (for pass 2);
-// cnt: per-bucket totals.  Both are zero between uses (the last CTA resets).
-template <class Src>
 // <= 48 registers (5 CTAs per SM worth): a CTA fits beside the two CTAs of
 // the epoch kernel (scd.cu, 104 registers), so the next round's permutation
 // runs under the epoch (GLM_PERM_LEAN overrides for experiments)
@@ -435,6 +432,10 @@ template <class Src>
 #define GLM_PERM_LEAN 5
 #endif
 #define PERM_BOUNDS __launch_bounds__(PERM_THREADS, GLM_PERM_LEAN)
+
+// Pass 1.  ctl: [0] ticket, [1] overflow count, [2] overflow total (for pass 2);
+// cnt: per-bucket totals.  Both are zero between uses (the last CTA resets).
+template <class Src>
 __global__ void PERM_BOUNDS region_scatter_kernel(
     Src src, int64_t n, int nb, uint32_t cap, uint32_t *cnt, uint32_t *boff, uint32_t *ctl,
     uint64_t *region, uint64_t *ovf, uint32_t *ovf_b) {
