@@ -9,7 +9,8 @@ import paper_1803_06333_b200 as g
 from paper_1803_06333_b200 import _lib as L
 from paper_1803_06333_b200.data import DeviceMatrix
 torch.cuda.set_device(0)
-indptr, rows, vals, y = bench.gen_columns(0, bench.N_EX // bench.BLOCK)
+# SHARE=k: the 1/k share of the examples one rank owns at k GPUs
+indptr, rows, vals, y = bench.gen_columns(0, (bench.N_EX // bench.BLOCK) // int(os.environ.get("SHARE", "1")))
 dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
 spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, bench.N_EX, bench.D_FEAT)
 eng = g.Engine(dm, spec, g.HierarchyConfig(t1=10**6, seed=0, epochs=1), mode="async",

@@ -17,7 +17,8 @@ world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK",
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
 if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
-per = (bench.N_EX // bench.BLOCK) // world
+# SHARE=k (one process): the 1/k share of the examples one rank owns at k GPUs
+per = (bench.N_EX // bench.BLOCK) // (world if world > 1 else int(os.environ.get("SHARE", "1")))
 indptr, rows, vals, y = bench.gen_columns(rank * per, (rank + 1) * per)
 dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
 spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, bench.N_EX, bench.D_FEAT)
