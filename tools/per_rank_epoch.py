@@ -12,7 +12,9 @@ import paper_1803_06333_b200 as g
 from paper_1803_06333_b200.data import DeviceMatrix
 
 torch.cuda.set_device(0)
-for n_gpus in (1, 2, 4, 8):
+SHARES = [int(x) for x in os.environ.get("SHARES", "1,2,4,8").split(",")]
+TRAJ = int(os.environ.get("TRAJ", "20"))
+for n_gpus in SHARES:
     blocks = (bench.N_EX // bench.BLOCK) // n_gpus
     indptr, rows, vals, y = bench.gen_columns(0, blocks)
     dm = DeviceMatrix.from_csc(bench.D_FEAT, indptr, rows, vals)
@@ -22,7 +24,7 @@ for n_gpus in (1, 2, 4, 8):
     for _ in range(3):
         eng.outer_round()
     wk = next(iter(eng.workers.values()))
-    traj = 20
+    traj = TRAJ
     eng.reset()
     graph = eng.capture(traj)
     best = 1e9
@@ -44,7 +46,7 @@ for n_gpus in (1, 2, 4, 8):
     torch.cuda.synchronize()
     k_ms, k_n = wk.solver.timing_read()
     wk.solver.timing(False)
-    print(json.dumps({"share_of_n_gpus": n_gpus, "examples": len(y), "step_ms": best,
+    print(json.dumps({"share_of_n_gpus": n_gpus, "examples": len(y), "traj": traj, "step_ms": best,
                       "epoch_ms": k_ms[1] / max(k_n, 1)}), flush=True)
     eng.close()
     del eng, dm
