@@ -16,14 +16,13 @@ constexpr int RED_THREADS = 256;
 // columns in flight (the reduction scratch holds up to 4096 CTA partials)
 template <class K>
 static int full_grid(K kernel) {
-    static int grid = 0;
-    if (!grid) {
+    static const int grid = [kernel] {        // thread-safe once-only initialisation
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, RED_THREADS, 0) !=
                 cudaSuccess || per_sm < 1)
             per_sm = 2;
-        grid = (per_sm > 8 ? 8 : per_sm) * NUM_SMS;
-    }
+        return (per_sm > 8 ? 8 : per_sm) * NUM_SMS;
+    }();
     return grid;
 }
 

@@ -41,6 +41,7 @@
 // SpMV (the reference recomputes it exactly, solver.py:300); the parity tests
 // bound the difference (tests/test_gpu_solver.py).
 
+#include <atomic>
 #include <cstdio>
 
 #include "solver.cuh"
@@ -1303,11 +1304,15 @@ static int grid_stride_blocks(int64_t n) {
 
 template <int G, int R, bool DENSE, int CM>
 static int launch_async_t(const EpochParams &p, int max_inflight, cudaStream_t s) {
-    static int blocks_per_sm = 0;   // identical for every B200
+    // identical for every B200; atomic because the reference calls the
+    // device solve from one thread per device (engine.py:259-263)
+    static std::atomic<int> occ{0};
+    int blocks_per_sm = occ.load(std::memory_order_relaxed);
     if (!blocks_per_sm) {
         GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &blocks_per_sm, scd_async<G, R, DENSE, CM>, 256, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
+        occ.store(blocks_per_sm, std::memory_order_relaxed);
     }
     // Staleness control: at most max_inflight coordinates in flight (default
     // n/32, i.e. ~3% of the partition) — the GPU analogue of the reference's
@@ -1404,11 +1409,13 @@ static int launch_narrow_t(const EpochParams &p, bool async, int64_t budget, dou
         GLM_CUDA_TRY(cudaGetLastError());
         return GLM_OK;
     }
-    static int blocks_per_sm = 0;
+    static std::atomic<int> occ{0};
+    int blocks_per_sm = occ.load(std::memory_order_relaxed);
     if (!blocks_per_sm) {
         GLM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
                                                                    scd_replica<R>, 256, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
+        occ.store(blocks_per_sm, std::memory_order_relaxed);
     }
     constexpr int W = 8;
     int64_t cap = (int64_t)blocks_per_sm * NUM_SMS;
@@ -1489,11 +1496,12 @@ static bool seq_csc_forced() {
 template <int BS, bool DENSE>
 static int launch_seq_t(const EpochParams &p, cudaStream_t s) {
     if (BS == 32 && !DENSE && p.d <= LVL_TAB_MAX && !seq_csc_forced()) {
-        static int dbg = -1;
-        if (dbg < 0) {
+        static std::atomic<int> dbg_set{-1};
+        if (dbg_set.load(std::memory_order_relaxed) < 0) {
             const char *e = getenv("GLM_LVL_DEBUG");
-            dbg = e && e[0] == '1';
+            int dbg = e && e[0] == '1';
             if (dbg) GLM_CUDA_TRY(cudaMemcpyToSymbol(lvl_debug, &dbg, sizeof(int)));
+            dbg_set.store(dbg, std::memory_order_relaxed);
         }
         const bool sv = p.d <= LVL_SMEM_VIEW_MAX;
         const size_t tab = (size_t)((p.d + 16) & ~15LL);
