@@ -392,10 +392,25 @@ def coordinate_update(spec, rows, vals, sqnorm, t_cur, view, quad):
 
 # --------------------------------------------------- reference-engine hook
 class _CtxCache:
+    """One device context per matrix.  The reference calls the hook from one
+    thread per device (engine.py:259-263): creation is locked, and calls on
+    one context are serialised by its own lock (calls on different contexts
+    run concurrently; ctypes releases the GIL)."""
+
     def __init__(self):
         self.ctx = {}
+        self.lock = threading.Lock()
+        self.call_locks = {}
+
+    def call_lock(self, data):
+        with self.lock:
+            return self.call_locks.setdefault(id(data), threading.Lock())
 
     def get(self, data):
+        with self.lock:
+            return self._get(data)
+
+    def _get(self, data):
         key = id(data)
         hit = self.ctx.get(key)
         if hit is not None and hit[0] is data:
@@ -468,8 +483,9 @@ def gpu_chunk_runner(mode=None, epochs=None):
         ep = cfg.epochs if epochs is None else epochs
         md = mode if mode is not None else mode_for_threads(cfg.threads_per_device)
         ctx = cache.get(sub.data)
-        delta, dv, values, info, scal, gs, dmp, st = device_solve_host(
-            ctx, sub, dev.gen.state, dev.damping.delta, ep, md)
+        with cache.call_lock(sub.data):
+            delta, dv, values, info, scal, gs, dmp, st = device_solve_host(
+                ctx, sub, dev.gen.state, dev.damping.delta, ep, md)
         dev.gen.state = gs
         dev.damping.delta = dmp
         if st != L.GLM_OK:

@@ -240,6 +240,50 @@ def test_gpu_chunk_runner_drop_in(golden):
     runner.close()
 
 
+def test_gpu_chunk_runner_concurrent_devices(golden):
+    """The reference calls the hook from one thread per device
+    (engine.py:259-263): four devices' subtasks through one runner from four
+    threads at once give the same bits as one after another."""
+    from concurrent.futures import ThreadPoolExecutor
+    z = golden("solve")
+
+    class Cfg:
+        epochs = 3
+        threads_per_device = 1
+
+    def case(c):
+        p = f"c{c}_"
+        m = _mat(z, p)
+        tgt = z[p + "target"]
+        kind = KINDS[int(z[p + "kind"])]
+        spec = g.ObjectiveSpec(kind, float(z[p + "lam"]), 1, 1, target=tgt if len(tgt) else None)
+        return g.LocalSubproblem(spec=spec, lin=z[p + "lin"], quad=float(z[p + "quad"]),
+                                 const=float(z[p + "const"]), base=z[p + "base"], data=m,
+                                 col_ids=np.arange(m.n_cols)), int(z[p + "gen_seed"])
+
+    subs = [case(c % int(z["n_cases"])) for c in range(4)]
+
+    class Dev:
+        pass
+
+    def run(runner, i):
+        sub, seed = subs[i]
+        dev = Dev()
+        dev.gen = g.PermutationGenerator(seed)
+        dev.damping = g.DampingState()
+        res = runner(sub, dev, Cfg())
+        return res.delta_alpha.tobytes(), res.delta_v.tobytes(), dev.gen.state
+
+    r1 = g.gpu_chunk_runner()
+    seq = [run(r1, i) for i in range(4)]
+    r1.close()
+    r2 = g.gpu_chunk_runner()
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(lambda i: run(r2, i), range(4)))
+    r2.close()
+    assert par == seq
+
+
 def test_gpu_chunk_runner_retries_vs_oracle(golden):
     """Rejected attempts through glm_device_solve: a caller-held damping above 1
     overshoots, the solve rolls back, halves and retries (solver.py:281-300);
