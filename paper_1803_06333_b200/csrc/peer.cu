@@ -352,9 +352,12 @@ __global__ void __launch_bounds__(PEER_THREADS) round_start_kernel(RoundStart p)
 // P1 -> P2 is a grid barrier on st->turn (the deciding block bumps it), P1 ->
 // P3 is the ranks' publication flags (ours is released only after all our
 // blocks arrived in P1).  Blocks spin only on work that finishes
-// independently of them and the grid is small (2 blocks per SM), so every
-// block becomes resident.  Replaces value + finalize + round start: three
-// kernel launches, ramps and tails per round become one.
+// independently of them and the grid is sized from the occupancy (1 block per
+// SM for a short Delta v, 2 for a long one; glm_peer_create), so every block
+// becomes resident; every spin has a %globaltimer deadline.  Block 0 resets
+// the solver state for the next round as soon as every block has read the
+// decision.  Replaces value + finalize + round start: three kernel launches,
+// ramps and tails per round become one.
 // decide_attempt (scd.cu) from state loaded up front: the fold's loads and
 // the state's loads share one round trip.  Returns 0 when the attempt was
 // rejected (the view goes back to the snapshot), else 1.
