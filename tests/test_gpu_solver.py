@@ -49,7 +49,10 @@ def test_permutation_stream_bit_exact(golden):
 def test_permutation_large_vs_oracle():
     # row-count argsort up to 2^21 keys, global-bucket argsort above
     for seed, n in [(5, 1), (6, 2), (7, 4095), (11, 131_073), (13, 1_000_003), (17, 1 << 21),
-                    (19, (1 << 21) + 1)]:
+                    (19, (1 << 21) + 1),
+                    # bucket-count and key-block boundaries of the region generator
+                    (23, 512), (29, 513), (31, 1024), (37, 4096), (41, 4097), (43, 1 << 20),
+                    (47, (1 << 20) + 1)]:
         gen = g.PermutationGenerator(seed)
         got = gen.permute(n)
         want, st = oracle.permute(seed, n)
