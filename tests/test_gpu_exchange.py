@@ -62,6 +62,28 @@ def test_fused_round_bit_identical_single_gpu(kind, retry_budget):
     np.testing.assert_allclose(runs[1].trace.objectives(), want["objective"], rtol=1e-10)
 
 
+def test_fused_round_long_delta_v_bit_identical():
+    """A Delta v of 2^20 + 3 rows: the turn runs two blocks per SM with every
+    row pass of P1 and P3 taking several rows per thread — the same bits as
+    the unfused rounds, and the oracle's trace (C4's 10M-row regime, small)."""
+    m = _synth(3_000, (1 << 20) + 3, 8, 7)
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    spec = g.ObjectiveSpec("dual_l2_logistic", 1.0, m.n_cols, m.n_rows)
+    cfg = g.HierarchyConfig(t1=4, seed=8, epochs=1)
+    runs = []
+    for peer in (False, True):
+        eng = g.Engine(m, spec, cfg, mode="sequential", sync_solves=False, retry_budget=0,
+                       peer_exchange=peer)
+        assert (eng.exchange is not None) == peer
+        runs.append(eng.train(g.StoppingCriteria(max_rounds=4)))
+        eng.close()
+    np.testing.assert_array_equal(runs[0].trace.objectives(), runs[1].trace.objectives())
+    np.testing.assert_array_equal(runs[0].model.alpha, runs[1].model.alpha)
+    np.testing.assert_array_equal(runs[0].v, runs[1].v)
+    want = oracle.train(om, 0, 1.0, epochs=1, seed=8, rounds=4)
+    np.testing.assert_allclose(runs[1].trace.objectives(), want["objective"], rtol=1e-10)
+
+
 def test_fused_round_reset_and_graph_replay():
     """reset() drops the pending Delta v; a captured graph of fused rounds
     replays to the same trajectory as eager rounds."""
