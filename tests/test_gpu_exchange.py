@@ -156,6 +156,19 @@ def test_two_process_exchange_same_gpu(rs):
         out.stdout[-2000:]
 
 
+@pytest.mark.parametrize("rs", ["0", "1"])
+def test_three_process_exchange_same_gpu(rs):
+    """Three ranks on cuda:0: an odd world, and with rs = 1 the reduce-scatter
+    slices 1024 / 1024 / 952 rows of the 3000-row Delta v (a ragged last slice)
+    — bit-identical to the deterministic reducer and the in-process K = 3
+    engine."""
+    out = _torchrun("--same-gpu", nproc=3, env={"GLM_PEER_RS": rs})
+    assert out.returncode == 0, _why(out)
+    assert "EXCHANGE OK" in out.stdout, out.stdout[-2000:]
+    assert "GRAPH sequential OK" in out.stdout and "GRAPH async OK" in out.stdout, \
+        out.stdout[-2000:]
+
+
 def test_dead_rank_surfaces_as_error():
     """Rank 1 dies mid-training; rank 0's device-side waits hit their deadline
     (3 s here; the reference's DEFAULT_TIMEOUT is 60 s, comm.py:30) and the
