@@ -34,16 +34,22 @@ def _synth(n, d, k, seed):
 
 
 @pytest.mark.parametrize("retry_budget", [4, 0])
-@pytest.mark.parametrize("kind", ["dual_l2_logistic", "dual_l2_svm", "ridge_primal"])
+@pytest.mark.parametrize("kind", ["dual_l2_logistic", "dual_l2_svm", "ridge_primal",
+                                  "lasso_primal", "logistic_primal"])
 def test_fused_round_bit_identical_single_gpu(kind, retry_budget):
     """retry_budget 0: one attempt per round, the round ends in glm_round_turn
     (value + finalize + exchange + next round start in one kernel)."""
+    from paper_1803_06333_b200.objectives import KINDS
     m = _synth(6_000, 900, 8, 3)
     om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
-    if kind == "ridge_primal":
+    if kind in ("ridge_primal", "lasso_primal"):
         tgt = np.random.default_rng(1).standard_normal(m.n_rows)
         spec = g.ObjectiveSpec(kind, 1.0, m.n_rows, m.n_cols, target=tgt)
-        k = 2
+        k = KINDS.index(kind)
+    elif kind == "logistic_primal":
+        tgt = np.where(np.random.default_rng(1).standard_normal(m.n_rows) >= 0, 1.0, -1.0)
+        spec = g.ObjectiveSpec(kind, 1.0, m.n_rows, m.n_cols, target=tgt)
+        k = KINDS.index(kind)
     else:
         tgt = None
         spec = g.ObjectiveSpec(kind, 1.0, m.n_cols, m.n_rows)
