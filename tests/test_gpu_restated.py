@@ -61,6 +61,30 @@ def test_engine_trace_vs_oracle(kind):
 
 
 @pytest.mark.parametrize("kind", KINDS)
+def test_fused_round_vs_oracle(kind):
+    """One attempt per round ending in the fused round turn (value, damping
+    decision, Delta v exchange, next round's model in one kernel): the same
+    bits as the unfused rounds and the oracle's trace, for every restated kind
+    (their f terms run inside the turn's P1 and P3)."""
+    m, spec = _problem(kind, seed=2)
+    om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
+    kw = dict(target=spec.row_target, y=spec.coord_target, rho=spec.l1_ratio)
+    cfg = g.HierarchyConfig(t1=6, seed=7, epochs=1)
+    runs = []
+    for peer in (False, True):
+        eng = g.Engine(m, spec, cfg, mode="sequential", sync_solves=False, retry_budget=0,
+                       peer_exchange=peer)
+        assert (eng.exchange is not None) == peer
+        runs.append(eng.train(g.StoppingCriteria(max_rounds=6)))
+        eng.close()
+    np.testing.assert_array_equal(runs[0].trace.objectives(), runs[1].trace.objectives())
+    np.testing.assert_array_equal(runs[0].model.alpha, runs[1].model.alpha)
+    np.testing.assert_array_equal(runs[0].v, runs[1].v)
+    ref = oracle.train(om, kind, spec.lam, epochs=1, seed=7, rounds=6, **kw)
+    np.testing.assert_allclose(runs[1].trace.objectives(), ref["objective"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("kind", KINDS)
 def test_damped_solve_vs_oracle(kind):
     m, spec = _problem(kind, seed=1)
     om = oracle.OMatrix(m.n_rows, m.indptr, m.rows, m.vals)
