@@ -121,3 +121,24 @@ def test_narrow_async_wide_views(d):
     assert np.all(np.diff(res.epoch_values) <= 0)
     dv = oracle.matvec(om, np.asarray(res.delta_alpha))
     assert np.max(np.abs(np.asarray(res.delta_v) - dv)) < 1e-9 * max(1.0, np.max(np.abs(dv)))
+
+
+def test_narrow_dual_ridge_async_reaches_target_like_sequential():
+    """C1 as BASELINE words it (ridge in the dual), scaled down: 6000 examples
+    x 200 features, coordinates = examples on the narrow replica kernel. The
+    async run reaches the deterministic run's 1e-3 gap target within +-10 %
+    epochs."""
+    rng = np.random.default_rng(12)
+    n_ex, n_feat = 6_000, 200
+    X = rng.standard_normal((n_ex, n_feat)) / np.sqrt(n_feat)
+    b = X @ rng.standard_normal(n_feat) + 0.1 * rng.standard_normal(n_ex)
+    m = g.DenseColumnMatrix(X.T)                        # column j = example j
+    spec = g.ObjectiveSpec("dual_ridge", 1.0, n_ex, n_feat, target=b)
+    runs = {}
+    for mode in ("sequential", "async"):
+        eng = g.Engine(m, spec, g.HierarchyConfig(t1=30, seed=3, epochs=1), mode=mode)
+        res = eng.train(g.StoppingCriteria(max_rounds=30))
+        runs[mode] = _epochs_to(res.trace.gaps(), res.trace.objectives(), 1e-3)
+    assert runs["sequential"] is not None and runs["async"] is not None, runs
+    assert abs(runs["async"] - runs["sequential"]) <= max(1, round(0.1 * runs["sequential"])), \
+        runs
