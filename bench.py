@@ -317,16 +317,20 @@ def ours_main(args):
     # event-timed segments.  With --graph (default) each trajectory is one CUDA
     # graph (rounds + NCCL all-reduce captured); the library's per-attempt
     # timing events are captured as event-record nodes and re-read per replay.
-    traj = args.traj
+    # exactly K = --steps timed rounds: n_seg trajectories of traj rounds and,
+    # when traj does not divide K, one shorter trajectory of the remainder
+    traj = max(1, min(args.traj, args.steps))
     n_seg = max(1, args.steps // traj)
-    steps_timed = n_seg * traj
+    rem = max(0, args.steps - n_seg * traj)
+    steps_timed = n_seg * traj + rem
     for _ in range(args.warmup):
         eng.outer_round()
     torch.cuda.synchronize()
     eng.check_solves()
     wk.solver.timing_read()                     # drop warm-up events
-    graph = graph_inst = None
+    graph = graph_inst = graph_rem = None
     launches_per_traj = None
+    launches_rem = 0
     if args.graph:
         # two captures of the same trajectory: the timed one without any
         # instrumentation, and one with the library's per-kernel CUDA events
@@ -336,19 +340,25 @@ def ours_main(args):
             c0 = lib.glm_launch_count()
             graph = eng.capture(traj)
             launches_per_traj = lib.glm_launch_count() - c0
+            if rem:
+                eng.reset()
+                c0 = lib.glm_launch_count()
+                graph_rem = eng.capture(rem)
+                launches_rem = lib.glm_launch_count() - c0
             eng.reset()
             wk.solver.timing(True)
             graph_inst = eng.capture(traj)
             wk.solver.timing(False)
         except Exception as exc:   # pragma: no cover - capture unsupported
             print(f"graph capture failed ({exc!r}); timing eager rounds", file=sys.stderr)
-            graph = graph_inst = None
+            graph = graph_inst = graph_rem = None
             wk.solver.timing(False)
             wk.solver.timing_read()
             torch.cuda.synchronize()
 
-    def run_traj(g=None):
+    def run_traj(g=None, rounds=None):
         g = graph if g is None else g
+        rounds = traj if rounds is None else rounds
         eng.reset()
         if world > 1:
             torch.distributed.barrier()
@@ -359,7 +369,7 @@ def ours_main(args):
         if g is not None:
             g.replay()
         else:
-            for _ in range(traj):
+            for _ in range(rounds):
                 eng.outer_round()
         t1.record(stream)
         torch.cuda.synchronize()
@@ -387,6 +397,8 @@ def ours_main(args):
         seg_ms = 0.0
         for _ in range(n_seg):
             seg_ms += run_traj()
+        if rem:
+            seg_ms += run_traj(graph_rem, rounds=rem)
         launches = lib.glm_launch_count() - launches0
         inst_ms = 0.0
         if graph_inst is not None:           # the per-kernel breakdown, after the timing
@@ -402,9 +414,9 @@ def ours_main(args):
             k_ms, attempts = wk.solver.timing_read()
             kern_ms += k_ms
             wk.solver.timing(False)
-            launches -= n_seg * len(eng.workers)       # set_state kernels of the resets
+            launches -= (n_seg + (1 if rem else 0)) * len(eng.workers)   # resets' set_state
         else:
-            launches = launches_per_traj * n_seg
+            launches = launches_per_traj * n_seg + launches_rem
     ms_total = max_over_ranks(seg_ms, world)
     eng.check_solves()
     res_state, _ = wk.solver.result()
@@ -513,7 +525,7 @@ def ours_main(args):
         print(json.dumps(line), flush=True)
     # Normal interpreter exit (atexit hooks run): drop the captured graphs and
     # engines first, then tear the process group down on every rank together.
-    del graph, graph_inst
+    del graph, graph_inst, graph_rem
     torch.cuda.synchronize()
     for e in (eng, eng2):
         if e is not None:
